@@ -1,0 +1,380 @@
+"""Pins of the oracle against what the paper and the mathematics fix (CPU only).
+
+Each test names the passage it pins.  None of them re-types the oracle's
+formula: the pins are worked examples (SPEC.md / hand-derived fractions in
+tests/golden/), closed forms, identities, a dense W S W^T brute force built
+from the explicit periodic B-spline definition, and invariants the paper
+states (partition of unity, spatial symmetry, exactness of the sum).
+"""
+import json
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "single_particle.json")))
+
+
+def slot(d, R):
+    L = 2 * R + 1
+    return ((d[0] + R) * L + (d[1] + R)) * L + (d[2] + R)
+
+
+def lin(g, n):
+    return (g[0] * n[1] + g[1]) * n[2] + g[2]
+
+
+# ----------------------------------------------------------------- locate (R5)
+@pytest.mark.parametrize("x,h,cell,xi", [
+    (2.25, 1.0, 2, 0.25),
+    (3.0, 1.0, 3, 0.0),        # SPEC.md:47 (a node maps to the upper cell)
+    (1.75, 0.5, 3, 0.5),
+])
+def test_locate_spec_examples(x, h, cell, xi):
+    c, f = oracle.locate([x, 0.0, 0.0], n=(8, 8, 8), h=(h, 1.0, 1.0))
+    assert c[0] == cell and f[0] == xi
+
+
+def test_locate_domain_errors():
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.locate([8.0, 0.0, 0.0], n=(8, 8, 8))
+    assert e.value.code == oracle.OR_ERR_DOMAIN
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.locate([-1e-300, 0.0, 0.0], n=(8, 8, 8))
+    assert e.value.code == oracle.OR_ERR_DOMAIN
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.locate([float("nan"), 0.0, 0.0], n=(8, 8, 8))
+    assert e.value.code == oracle.OR_ERR_NONFINITE
+    # slab ownership: cell 2 is outside [3, 6)
+    with pytest.raises(oracle.OracleError):
+        oracle.locate([2.5, 0.0, 0.0], n=(8, 8, 8), x_begin=3, x_end=6)
+
+
+# ----------------------------------------------------------- shape functions
+def test_phi_values():
+    # SPEC.md:111-113; order-2 values follow from the quadratic B-spline (R3)
+    assert oracle.phi(1, 0.0) == 1.0
+    assert oracle.phi(2, 0.0) == 0.75
+    assert oracle.phi(2, 1.0) == 0.125
+    assert oracle.phi(2, 1.5) == 0.0 and oracle.phi(1, 1.0) == 0.0
+
+
+@pytest.mark.parametrize("order,xi,base,w", [
+    (1, 0.25, 0, [0.75, 0.25]),
+    (2, 0.0, -1, [0.125, 0.75, 0.125]),
+    (2, 0.25, -1, [1 / 32, 11 / 16, 9 / 32]),   # hand-derived (golden order2 x-axis)
+    (2, 0.5, 0, [0.5, 0.5, 0.0]),               # tie -> ">=" branch, PAPER.md:168 (R4)
+    (2, 0.3, -1, None),
+    (2, 0.7, 0, None),
+])
+def test_support_and_weights(order, xi, base, w):
+    b, ww = oracle.support_1d(order, xi)
+    assert b == base
+    if w is not None:
+        assert list(ww) == w
+
+
+def test_partition_of_unity_and_nonnegativity():
+    # sum_g W_pg = 1, W >= 0
+    rng = np.random.default_rng(1)
+    for order in (1, 2):
+        for xi in rng.random(2000):
+            _, w = oracle.support_1d(order, float(xi))
+            assert (w >= 0).all()
+            assert abs(w.sum() - 1.0) <= 4.5e-16     # a few ulp of 1
+    # 2D product example SPEC.md:131: (0.25, 0.5) -> (.375, .375, .125, .125)
+    _, wx = oracle.support_1d(1, 0.25)
+    _, wy = oracle.support_1d(1, 0.5)
+    assert list(np.outer(wx, wy).ravel()) == [0.375, 0.375, 0.125, 0.125]
+
+
+# ------------------------------------------------------------------ alpha
+def test_alpha_closed_forms():
+    # PAPER.md:91-96
+    assert (oracle.alpha([0, 0, 0]) == np.eye(3)).all()
+    assert (oracle.alpha([0, 0, 1]) == 0.5 * np.array([[1, 1, 0], [-1, 1, 0], [0, 0, 2]])).all()
+    assert (oracle.alpha([1, 1, 1]) == 0.25 * np.array([[2, 2, 0], [0, 2, 2], [2, 0, 2]])).all()
+
+
+def test_alpha_is_inverse_of_I_plus_cross():
+    # alpha = (I + C(omega))^-1 with C(omega) u = omega x u (reading R8); C built from np.cross,
+    # the inverse by LAPACK — an independent route to eq_alpha_matrix.
+    rng = np.random.default_rng(2)
+    for om in rng.normal(size=(2000, 3)) * 2.0:
+        C = np.stack([np.cross(om, e) for e in np.eye(3)], axis=1)
+        a = oracle.alpha(om)
+        assert np.abs(a @ (np.eye(3) + C) - np.eye(3)).max() < 1e-14
+        assert np.abs(a - np.linalg.inv(np.eye(3) + C)).max() < 1e-14
+        assert (oracle.alpha(-om) == a.T).all()       # alpha(-omega) = alpha(omega)^T exactly
+
+
+# --------------------------------------------------- single-particle goldens
+def _frac(v):
+    return float(Fraction(v[0], v[1]))
+
+
+@pytest.mark.parametrize("key", ["order1", "order2"])
+def test_single_particle_golden(key):
+    gd = GOLD[key]
+    order = 1 if key == "order1" else 2
+    n = gd["grid"]
+    out = oracle.assemble(n, order, 9, [gd["x"]], [gd["q"]], [gd["B"]])
+    g = lin(gd["node"], n)
+    d0 = slot((0, 0, 0), order)
+    for c, v in gd["diag"].items():
+        assert out[g, d0, int(c)] == _frac(v)
+    for c, v in gd["row_sum"].items():
+        assert out[g, :, int(c)].sum() == _frac(v)
+    assert np.count_nonzero(out) == gd["nonzeros"]
+    assert out[:, :, 8].sum() == gd["total_comp8"]
+    assert oracle.keys(n, order, [gd["x"]], [gd["q"]], [gd["B"]])[0] == gd["sort_key"]
+
+
+def test_cic_1d_spec_example():
+    gd = GOLD["cic_1d_spec"]
+    n = gd["grid"]
+    out = oracle.assemble(n, 1, 1, [gd["x"]], [gd["q"]])
+    for node, d, v in gd["entries"]:
+        assert out[lin(node, n), slot(d, 1), 0] == v
+    assert np.count_nonzero(out) == len(gd["entries"])
+
+
+# ------------------------------------------------------ dense brute force
+def dense_W(n, pos, order):
+    """W[g, p] = prod_mu phi(t_mu) with t the periodic-image distance in cell units
+    (eq_weight_matrix PAPER.md:123-128 with eq_shape_bspline); phi written from its
+    textbook piecewise definition, independent of the oracle."""
+    n = np.asarray(n)
+    gs = np.stack(np.meshgrid(*[np.arange(k) for k in n], indexing="ij"), -1).reshape(-1, 3)
+    t = pos[None, :, :] - gs[:, None, :]
+    t = (t + n / 2) % n - n / 2            # nearest periodic image
+    a = np.abs(t)
+    if order == 1:
+        f = np.clip(1 - a, 0, None)
+    else:
+        f = np.where(a <= 0.5, 0.75 - a ** 2, np.where(a <= 1.5, 0.5 * (1.5 - a) ** 2, 0.0))
+    return f.prod(-1)
+
+
+def stencil_to_dense(out, n, order):
+    R = order
+    nn = int(np.prod(n))
+    C = out.shape[2]
+    D = np.zeros((C, nn, nn))
+    rng = range(-R, R + 1)
+    gs = np.stack(np.meshgrid(*[np.arange(k) for k in n], indexing="ij"), -1).reshape(-1, 3)
+    for g, gv in enumerate(gs):
+        for dx in rng:
+            for dy in rng:
+                for dz in rng:
+                    h = ((gv[0] + dx) % n[0], (gv[1] + dy) % n[1], (gv[2] + dz) % n[2])
+                    D[:, g, lin(h, n)] += out[g, slot((dx, dy, dz), R)]
+    return D
+
+
+@pytest.mark.parametrize("order,n,np_", [(1, (4, 4, 4), 300), (1, (3, 5, 4), 200), (2, (5, 5, 5), 300),
+                                          (2, (6, 5, 7), 200)])
+def test_dense_brute_force(order, n, np_):
+    # eq_D_WSW: M^{ij} = W S^{ij} W^T, S^{ij} = diag(q alpha^{ij}),
+    # alpha via LAPACK inverse of (I + C(omega)).
+    d = synth.random_particles(n, np_, seed=7 + order, bscale=2.0, qrange=(-1.5, 1.5))
+    out = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    W = dense_W(n, d["pos"], order)
+    s = np.empty((np_, 9))
+    for p in range(np_):
+        om = d["B"][p] / 2.0
+        C = np.stack([np.cross(om, e) for e in np.eye(3)], axis=1)
+        s[p] = (d["q"][p] * np.linalg.inv(np.eye(3) + C)).ravel()
+    D = stencil_to_dense(out, n, order)
+    scale = np.abs(W).sum(0).max() ** 2 * np.abs(s).max()
+    for c in range(9):
+        ref = (W * s[:, c]) @ W.T
+        assert np.abs(D[c] - ref).max() <= 1e-13 * scale, c
+    # row sparsity bound: at most (2n+1)^3 nonzeros per row
+    assert (np.count_nonzero(D[0], axis=1) <= (2 * order + 1) ** 3).all()
+
+
+# ------------------------------------------------------------- invariants
+def _cfg_particles(order, n=(6, 5, 7), ppc=6, seed=11):
+    cfg = synth.Config("t", n, order, "tensor", ppc, seed=seed)
+    return synth.particles(cfg)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_partition_of_unity_moment(order):
+    # PAPER.md:164 with eq_mass_matrix_general: sum_{g'} M^{ij}_{gg'} = sum_p s_p^{ij} W_pg.
+    n = (6, 5, 7)
+    d = _cfg_particles(order, n)
+    out = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    W = dense_W(n, d["pos"], order)
+    s = np.stack([d["q"][p] * oracle.alpha(d["B"][p] / 2).ravel() for p in range(len(d["q"]))])
+    mom = W @ s
+    assert np.abs(out.sum(1) - mom).max() <= 1e-13 * np.abs(mom).max()
+    assert np.abs(out.sum((0, 1)) - s.sum(0)).max() <= 1e-12 * np.abs(s).sum()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_spatial_symmetry_bit_exact(order):
+    # eq_spatial_symmetry: out[g][d][ij] == out[g+d][-d][ij] exactly
+    n = (6, 5, 7)
+    d = _cfg_particles(order, n)
+    out = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    R = order
+    gs = np.stack(np.meshgrid(*[np.arange(k) for k in n], indexing="ij"), -1).reshape(-1, 3)
+    rr = range(-R, R + 1)
+    for dd in [(a, b, c) for a in rr for b in rr for c in rr]:
+        nb = np.array([lin(((g[0] + dd[0]) % n[0], (g[1] + dd[1]) % n[1], (g[2] + dd[2]) % n[2]), n)
+                       for g in gs])
+        assert (out[:, slot(dd, R)] == out[nb, slot(tuple(-x for x in dd), R)]).all()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_B_reversal_transposes_components(order):
+    # alpha(-omega) = alpha(omega)^T (eq_alpha_matrix) => M^{ij}(B) = M^{ji}(-B)
+    n = (5, 5, 5)
+    d = _cfg_particles(order, n)
+    a = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    b = oracle.assemble(n, order, 9, d["pos"], d["q"], -d["B"])
+    assert (a.reshape(-1, 3, 3) == b.reshape(-1, 3, 3).transpose(0, 2, 1)).all()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_B_zero_reduces_to_scalar(order):
+    # alpha = I when B = 0 (eq_alpha_matrix) => M = M_scalar (x) I
+    n = (5, 6, 5)
+    d = _cfg_particles(order, n)
+    t = oracle.assemble(n, order, 9, d["pos"], d["q"], np.zeros_like(d["B"]))
+    s = oracle.assemble(n, order, 1, d["pos"], d["q"])
+    for c in range(9):
+        if c in (0, 4, 8):
+            assert (t[:, :, c] == s[:, :, 0]).all()
+        else:
+            assert (t[:, :, c] == 0).all()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_linearity_and_charge_scaling(order):
+    n = (5, 5, 6)
+    d = _cfg_particles(order, n)
+    full = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    h = len(d["q"]) // 3
+    a = oracle.assemble(n, order, 9, d["pos"][:h], d["q"][:h], d["B"][:h])
+    b = oracle.assemble(n, order, 9, d["pos"][h:], d["q"][h:], d["B"][h:])
+    assert np.abs(a + b - full).max() <= 1e-13 * np.abs(full).max()
+    acc = oracle.assemble(n, order, 9, d["pos"][h:], d["q"][h:], d["B"][h:], out=a.copy(), accumulate=True)
+    assert np.abs(acc - full).max() <= 1e-13 * np.abs(full).max()
+    two = oracle.assemble(n, order, 9, d["pos"], 2 * d["q"], d["B"])
+    assert (two == 2 * full).all()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_translation_by_one_cell(order):
+    n = (5, 6, 7)
+    d = _cfg_particles(order, n)
+    lattice = synth.particles(synth.Config("t", n, order, "tensor", 3, seed=5), lattice=True)
+    for dd in (d, lattice):
+        base = oracle.assemble(n, order, 9, dd["pos"], dd["q"], dd["B"])
+        sh = dd["pos"].copy()
+        sh[:, 1] = (sh[:, 1] + 1.0) % n[1]
+        moved = oracle.assemble(n, order, 9, sh, dd["q"], dd["B"])
+        b4 = base.reshape(n[0], n[1], n[2], -1)
+        m4 = moved.reshape(n[0], n[1], n[2], -1)
+        tol = 0 if dd is lattice else 1e-13 * np.abs(base).max()
+        assert np.abs(np.roll(b4, 1, axis=1) - m4).max() <= tol
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_permutation_invariance(order):
+    n = (5, 5, 5)
+    d = _cfg_particles(order, n)
+    a = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    p = np.random.default_rng(3).permutation(len(d["q"]))
+    b = oracle.assemble(n, order, 9, d["pos"][p], d["q"][p], d["B"][p])
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(a).max()
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_lattice_inputs_order_independent_exactly(order):
+    # dyadic lattice: every product and partial sum is exact, so any summation order gives the
+    # same bits (the property the GPU lattice parity test relies on)
+    n = (5, 5, 5)
+    d = synth.particles(synth.Config("t", n, order, "tensor", 8, seed=9), lattice=True)
+    a = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    p = np.random.default_rng(4).permutation(len(d["q"]))
+    b = oracle.assemble(n, order, 9, d["pos"][p], d["q"][p], d["B"][p])
+    assert (a == b).all()
+    W = dense_W(n, d["pos"], order)
+    s = np.stack([d["q"][i] * oracle.alpha(d["B"][i] / 2).ravel() for i in range(len(d["q"]))])
+    D = stencil_to_dense(a, n, order)
+    for c in (0, 1, 5, 8):
+        assert (D[c] == (W * s[:, c]) @ W.T).all()
+
+
+# --------------------------------------------------------------------- sort
+def test_sort_spec_example():
+    # particles in cells [2,0,2,1] -> order [1,3,0,2]
+    n = (5, 5, 5)
+    pos = np.array([[2.5, 0.5, 0.5], [0.5, 0.5, 0.5], [2.25, 0.5, 0.5], [1.5, 0.5, 0.5]])
+    r = oracle.sort(n, 1, 1, pos, np.ones(4))
+    assert list(r["perm"]) == [1, 3, 0, 2]
+    cells = [lin((k, 0, 0), n) for k in (0, 1, 2)]
+    assert [int(r["seg_count"][c]) for c in cells] == [1, 1, 2]
+    assert [int(r["seg_begin"][c]) for c in cells] == [0, 1, 2]
+
+
+@pytest.mark.parametrize("order,k", [(1, 4), (1, 8), (2, 4), (2, 8), (1, 1)])
+def test_sort_against_numpy_stable_argsort(order, k):
+    n = (6, 5, 7)
+    d = synth.random_particles(n, 2000, seed=21)
+    # repeat some particles to force equal keys
+    d["pos"][1000:1400] = d["pos"][:400]
+    r = oracle.sort(n, order, k, d["pos"], d["q"], d["B"])
+    key = oracle.keys(n, order, d["pos"], d["q"], d["B"])
+    ref = np.argsort(key, kind="stable")
+    perm = r["perm"]
+    assert sorted(perm[perm >= 0].tolist()) == list(range(2000))
+    assert (perm[perm >= 0] == ref).all()
+    counts = np.bincount(key, minlength=oracle.nbins(n, order))
+    assert (r["seg_count"] == counts).all()
+    padded = (counts + k - 1) // k * k
+    assert (r["seg_begin"] == np.concatenate([[0], np.cumsum(padded)])).all()
+    assert r["np_padded"] == padded.sum()
+    rec = r["rec"]
+    assert (rec[perm < 0] == 0).all()
+    src = perm[perm >= 0]
+    assert (rec[perm >= 0, 3] == d["q"][src]).all()
+    assert (rec[perm >= 0, 4:7] == d["B"][src]).all()
+    u = d["pos"][src] / 1.0
+    assert (rec[perm >= 0, :3] == u - np.floor(u)).all()
+
+
+def test_keys_group_support_identity():
+    # eq_group_partition: equal key <=> identical support node set.  For TSC the
+    # 3-node window of an axis is centred on the nearest node, so the support set is
+    # identified by the nearest node (axis 0 unwrapped, reading R12).
+    n = (6, 6, 6)
+    d = synth.random_particles(n, 3000, seed=3)
+    key = oracle.keys(n, 2, d["pos"], d["q"], d["B"])
+    centre = np.floor(d["pos"] + 0.5)
+    centre[:, 1:] %= np.asarray(n[1:])
+    ck = ((centre[:, 0] * n[1] + centre[:, 1]) * n[2] + centre[:, 2]).astype(np.int64)
+    pairs = set(zip(key.tolist(), ck.tolist()))
+    assert len({k for k, _ in pairs}) == len(pairs) == len({c for _, c in pairs})
+
+
+def test_sort_errors():
+    n = (5, 5, 5)
+    with pytest.raises(oracle.OracleError):
+        oracle.sort(n, 1, 4, [[5.0, 0, 0]], [1.0])
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.sort(n, 1, 4, [[1.0, 0, 0]], [float("inf")])
+    assert e.value.code == oracle.OR_ERR_NONFINITE
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.sort((4, 5, 5), 2, 4, [[1.0, 0, 0]], [1.0])
+    assert e.value.code == oracle.OR_ERR_INVALID_ARG
+    r = oracle.sort(n, 1, 4, np.zeros((0, 3)), np.zeros(0))
+    assert r["np_padded"] == 0 and (r["seg_count"] == 0).all()
