@@ -1,0 +1,374 @@
+#!/usr/bin/env python
+"""Benchmark of the ECSIM mass-matrix assembly hot path on B200 (one JSON line).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (weak scaling over x-slabs)
+
+A step = one pass of the whole hot path over one batch of synthetic particles
+already resident in HBM: mm_sort_by_cell (locate, key, histogram, padded scan,
+stable placement, record scatter) + mm_assemble (fused W/alpha, DMMA
+contraction, node-stencil scatter) [+ ghost exchange and mm_ghost_add at N>1].
+Workload at N=1: BASELINE config[1] "c2" (64^3, CIC, 64 ppc, random B, FP64
+tensor); N>1: weak scaling, one 64^3 x-slab per GPU of a (64N)x64x64 grid.
+The order-2 config c3 is measured the same way and reported under "order2".
+
+`--impl reference` times the oracle (plain FP64 CPU loop, oracle/) on the host
+cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "assembly Mparticles/s, B-spline order 1&2, 1/2/4/8 B200; % tensor/HBM roofline"
+UNIT = "Mparticles/s"
+HBM_BYTES_PER_PARTICLE_IN = 56.0   # x,y,z,q,Bx,By,Bz (FP64) read once
+
+
+def flops_per_particle(order, ncomp):
+    # F_method: 2 x (MMA entries per component issued by the tile plan) x C
+    entries = 64 if order == 1 else 640
+    return 2 * entries * ncomp
+
+
+def alg_bytes_per_particle(order, ncomp, ppc):
+    S = (2 * order + 1) ** 3
+    return (HBM_BYTES_PER_PARTICLE_IN if ncomp == 9 else 32.0) + S * ncomp * 8.0 / ppc
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f), "MEASURED_PEAKS.json"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "B200_PROFILING.md fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.lines = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_rate(cfg, d, budget_s=12.0):
+    """Oracle (plain single-thread FP64 C loop) on a bounded sample of the workload."""
+    import oracle
+    n = cfg.n
+    kind = cfg.ncomp
+    m = min(len(d["q"]), 20000)
+    t0 = time.perf_counter()
+    oracle.assemble(n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
+    t1 = time.perf_counter() - t0
+    # scale the sample to ~budget_s of CPU work (the output array memset is part of the oracle)
+    m2 = int(min(len(d["q"]), max(m, m * budget_s / max(t1, 1e-3))))
+    t0 = time.perf_counter()
+    oracle.assemble(n, cfg.order, kind, d["pos"][:m2], d["q"][:m2], d["B"][:m2] if kind == 9 else None)
+    t2 = time.perf_counter() - t0
+    return {"value": m2 / t2 / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {m2} of {len(d['q'])} particles of {cfg.name} (input order), whole {n} grid output,"
+                      f" {t2:.1f} s single-threaded on {os.cpu_count()} host cores"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.config("c2")
+    d = synth.particles(cfg)
+    import oracle
+    steps = []
+    m = 200000 // 4
+    for _ in range(args.warmup):
+        oracle.assemble(cfg.n, 1, 9, d["pos"][:m], d["q"][:m], d["B"][:m])
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        sl = slice((k * m) % (len(d["q"]) - m), (k * m) % (len(d["q"]) - m) + m)
+        oracle.assemble(cfg.n, 1, 9, d["pos"][sl], d["q"][sl], d["B"][sl])
+        steps.append(time.perf_counter() - t0)
+    t = float(np.sum(steps))
+    val = m * args.steps / t / 1e6
+    line = {"metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "c2: 64^3 periodic grid, CIC (order 1), 64 ppc, random B, FP64 tensor mass matrix",
+                       "sample_particles_per_step": m},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{m} particles per step of c2 (consecutive slices of the shuffled input), "
+                                       f"whole-grid output, single-threaded"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-order2", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+    import paper_2604_19286_b200 as mm
+    from paper_2604_19286_b200 import slab
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    mm.load_library(build_if_missing=False)
+    peaks, peak_src = load_peaks()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def setup(name):
+        base = synth.config(name)
+        if world == 1:
+            cfg, xb, xe = base, 0, base.n[0]
+        else:
+            cfg = synth.Config(base.name + f"-weak{world}", (base.n[0] * world, base.n[1], base.n[2]), base.order,
+                               base.kind, base.ppc, seed=base.seed)
+            xb, xe = rank * base.n[0], (rank + 1) * base.n[0]
+        d = synth.particles(cfg, xb, xe)
+        grid = mm.Grid(cfg.n, cfg.h, xb, xe)
+        dd = {k: torch.from_numpy(v).to(dev) for k, v in d.items()}
+        return cfg, grid, d, dd
+
+    def measure(name, with_extras):
+        cfg, grid, d, dd = setup(name)
+        order, kind = cfg.order, cfg.ncomp
+        sp = mm.Species(cfg.qom, cfg.dt, cfg.c, cfg.sigma)
+        out = torch.empty(mm.out_shape(grid, order, kind), dtype=torch.float64, device=dev)
+        ghost = torch.empty(mm.ghost_shape(grid, order, kind), dtype=torch.float64, device=dev) \
+            if mm.is_slab(grid) else None
+        plane_elems = grid.n[1] * grid.n[2] * (2 * order + 1) ** 3 * kind
+        widths = [cfg.n[0] // world] * world
+        state = {"h": None}
+        ev = []
+
+        def step(record=False):
+            state["h"] = mm.mm_sort_by_cell(grid, order, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"])
+            if record:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+            mm.mm_assemble(state["h"], kind, mm.MM_FP64, sp, out, ghost)
+            if record:
+                e1.record()
+                ev.append((e0, e1))
+            if world > 1:
+                slab.exchange_ghosts(out, ghost, order, plane_elems, rank, world, widths,
+                                     add=lambda k, src: mm.mm_ghost_add(grid, order, kind, out, src, k, 1))
+
+        for _ in range(args.warmup):
+            step()
+        barrier()
+        l0 = mm.launch_count()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            barrier()
+            t0.record()
+            for _ in range(args.steps):
+                step(record=True)
+            t1.record()
+            barrier()
+        launches = mm.launch_count() - l0
+        ms = t0.elapsed_time(t1)
+        if world > 1:
+            tt = torch.tensor([ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ms = float(tt.item())
+        asm_ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
+        npart = len(d["q"])
+        total = npart * world
+        res = {"cfg": cfg, "ms_per_step": ms / args.steps, "assemble_ms": asm_ms, "np": npart,
+               "value": total * args.steps / (ms / 1e3) / 1e6, "launches": launches, "clocks": clk.summary()}
+        # sort-only timing (same handle, same inputs)
+        if with_extras:
+            s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            s0.record()
+            for _ in range(max(5, args.steps // 10)):
+                state["h"] = mm.mm_sort_by_cell(grid, order, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"])
+            s1.record()
+            barrier()
+            res["sort_ms"] = s0.elapsed_time(s1) / max(5, args.steps // 10)
+        res["d"] = d
+        res["grid"], res["out"], res["ghost"], res["sp"], res["state"] = grid, out, ghost, sp, state
+        return res
+
+    r1 = measure("c2", True)
+    cfg = r1["cfg"]
+    ppc = synth.ppc_of(cfg)
+    F = flops_per_particle(1, 9)
+    # dominant kernel: mm_assemble (zero-fill + DMMA assembly kernel), events on the launch stream
+    fp64_peak, fp64_src = None, None
+    probe = os.path.join(ROOT, "profiles", "peaks_fp64.json")
+    if os.path.exists(probe):
+        with open(probe) as f:
+            pk = json.load(f)
+        fp64_peak, fp64_src = pk.get("dmma_tflops"), "profiles/peaks_fp64.json (DMMA.8x8x4 probe, measured)"
+    if fp64_peak is None:
+        fp64_peak = peaks.get("bf16_tflops", 1590.0) * 40.0 / 2250.0
+        fp64_src = f"{peak_src} bf16 x nominal FP64/bf16 ratio 40/2250"
+    achieved = r1["np"] * F / (r1["assemble_ms"] / 1e3) / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("assemble_o1_bytes_per_launch")
+    roof = {"bound": "tensor", "kernel": "mm_assemble (k_asm_o1<9> FP64 DMMA + zero-fill)", "achieved": achieved,
+            "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
+            "peak_source": fp64_src, "alg_flops_per_particle": F,
+            "alg_bytes_per_particle": alg_bytes_per_particle(1, 9, ppc),
+            "hbm_achieved_gbs": r1["np"] * alg_bytes_per_particle(1, 9, ppc) / (r1["assemble_ms"] / 1e3) / 1e9,
+            "hbm_peak_gbs": peaks.get("hbm_gbs")}
+
+    line = {"metric": METRIC, "value": r1["value"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": r1["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": ("c2: 64^3 periodic grid, CIC (order 1), 64 ppc, random B, FP64 tensor mass matrix"
+                                    if world == 1 else
+                                    f"weak scaling: ({64 * world})x64x64 grid, one 64^3 x-slab per GPU, CIC, 64 ppc"),
+                       "grid": list(cfg.n), "order": 1, "kind": "tensor", "ppc": ppc, "particles": r1["np"] * world,
+                       "parallelism": f"x-slab x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs (940 MB) and output (510 MB) larger than the 126 MB L2; no flush",
+                       "k_pad": 4},
+            "roofline": roof, "gpu_launches": r1["launches"], "clocks": r1["clocks"],
+            "breakdown": {"sort_ms": r1.get("sort_ms"), "assemble_ms": r1["assemble_ms"],
+                          "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
+                          "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6}}
+
+    if not args.no_order2:
+        r2 = measure("c3", True)
+        F2 = flops_per_particle(2, 9)
+        a2 = r2["np"] * F2 / (r2["assemble_ms"] / 1e3) / 1e12
+        line["order2"] = {"workload": "c3: 64^3, TSC (order 2), 64 ppc, random B, FP64 tensor" if world == 1 else
+                          "c3 weak-scaled slabs", "value": r2["value"], "unit": UNIT, "ms_per_step": r2["ms_per_step"],
+                          "sort_ms": r2.get("sort_ms"), "assemble_ms": r2["assemble_ms"],
+                          "roofline": {"bound": "tensor", "achieved": a2, "peak": fp64_peak, "unit": "TFLOP/s",
+                                       "frac": a2 / fp64_peak, "alg_flops_per_particle": F2}}
+        del r2
+
+    # ---- end to end through the public API with host buffers (pinned), H2D + D2H in the timed region
+    if not args.no_e2e:
+        import torch as T
+        d = r1["d"]
+        hp = {k: T.from_numpy(v).pin_memory() for k, v in d.items()}
+        dd = {k: T.empty(v.shape, dtype=v.dtype, device=dev) for k, v in hp.items()}
+        host_out = T.empty(r1["out"].shape, dtype=T.float64).pin_memory()
+        grid, out, ghost, sp, state = r1["grid"], r1["out"], r1["ghost"], r1["sp"], r1["state"]
+        ke = max(3, min(20, args.steps // 10))
+
+        def e2e_step():
+            for k in ("pos", "q", "B"):
+                dd[k].copy_(hp[k], non_blocking=True)
+            state["h"] = mm.mm_sort_by_cell(grid, 1, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"])
+            mm.mm_assemble(state["h"], 9, mm.MM_FP64, sp, out, ghost)
+            if world > 1:
+                slab.exchange_ghosts(out, ghost, 1, grid.n[1] * grid.n[2] * 27 * 9, rank, world,
+                                     [cfg.n[0] // world] * world,
+                                     add=lambda k, src: mm.mm_ghost_add(grid, 1, 9, out, src, k, 1))
+            host_out.copy_(out, non_blocking=True)
+
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        e0, e1 = T.cuda.Event(enable_timing=True), T.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(ke):
+            e2e_step()
+        e1.record()
+        barrier()
+        ems = e0.elapsed_time(e1)
+        if world > 1:
+            tt = T.tensor([ems], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            ems = float(tt.item())
+        h2d = sum(v.numel() * v.element_size() for v in hp.values())
+        line["e2e"] = {"value": r1["np"] * world * ke / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                       "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke,
+                       "note": "pinned host pos/q/B -> device, sort + assemble, full mass matrix -> pinned host"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = oracle_rate(cfg, r1["d"])
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

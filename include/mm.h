@@ -1,0 +1,202 @@
+/*
+ * mm.h — C ABI of the B200 (sm_100a) ECSIM mass-matrix assembly library
+ * (libmm.so).  arXiv 2604.19286, "Mass Matrix Assembly on Tensor Cores for
+ * Implicit Particle-In-Cell Methods".
+ *
+ * What it computes (eq_mass_matrix_ecsim / eq_alpha_matrix /
+ * eq_mass_matrix_general):
+ *
+ *   M^{ij}_{g g'} = sigma * sum_p s_p^{ij} W_pg W_pg'
+ *   s_p^{ij} = q_p alpha_p^{ij}            (MM_TENSOR, 9 components)
+ *            = q_p delta^{ij}              (MM_SCALAR, 1 component)
+ *   alpha_p  = (I - C(omega_p) + omega_p omega_p^T) / (1 + |omega_p|^2),
+ *   omega_p  = (qom * dt / 2) * B_p / c,   C(w) u = w x u
+ *   W_pg     = prod_mu phi^(n)((x_p^mu - x_g^mu) / h^mu)     (eq_shape_bspline)
+ *
+ * with first-order (CIC, n = 1) or second-order (TSC, n = 2) B-splines, via
+ * the paper's cell-local factorisation M = A B (eq_D_AB), particle batching
+ * in K_t = 4 (eq_D_batches) and the support-group decomposition
+ * (eq_group_partition), on FP64 DMMA tensor-core tiles.
+ *
+ * General conventions
+ *   - No CUDA or torch types cross this boundary.  Every pointer argument
+ *     documented as "device" is a CUDA device pointer on the current device;
+ *     "host" pointers are ordinary host memory.  Streams are passed as
+ *     `void*` holding a cudaStream_t (NULL = legacy default stream).
+ *   - Every entry point returns an mm_status; on failure a thread-local
+ *     message is available from mm_last_error().  No C++ exception crosses
+ *     the ABI.  Argument checks are synchronous.
+ *   - Grid geometry (readings R1, R2): node g sits at x = g*h,
+ *     cell c = [c*h, (c+1)*h); cells = nodes per axis, periodic along axes
+ *     1 and 2 always, and along axis 0 when the caller owns the whole axis
+ *     (x_begin == 0 && x_end == n[0]).  Linearisation is row-major, axis 0
+ *     slowest.
+ *   - Output layout: out[(g*S + slot)*C + comp] with
+ *       g    = ((ix - x_begin)*n[1] + iy)*n[2] + iz      (owned node rows)
+ *       S    = (2n+1)^3 = 27 (order 1) | 125 (order 2)  stencil slots
+ *       slot = ((dx+n)*(2n+1) + (dy+n))*(2n+1) + (dz+n), d = g' - g unwrapped
+ *       comp = 3*i + j (MM_TENSOR) | 0 (MM_SCALAR)
+ *     i.e. the full "27 neighbours x 9 components" (order 1) or
+ *     "125 x 9" (order 2) node-stencil block per node.
+ */
+#ifndef MM_H_
+#define MM_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MM_OK = 0,
+    MM_ERR_INVALID_ARG = 1,   /* bad pointer/size/enum/geometry                 */
+    MM_ERR_DOMAIN = 2,        /* a particle lies outside the owned cell slab   */
+    MM_ERR_NONFINITE = 3,     /* NaN/Inf in pos, q or B                        */
+    MM_ERR_INCOMPATIBLE = 4,  /* handle/order/kind/precision mismatch          */
+    MM_ERR_OUT_OF_MEMORY = 5, /* device allocation failed                      */
+    MM_ERR_CUDA = 6           /* CUDA runtime / launch error                   */
+} mm_status;
+
+typedef enum { MM_SCALAR = 1, MM_TENSOR = 9 } mm_kind; /* value = components C */
+
+typedef enum {
+    MM_FP64 = 0,   /* FP64 operands, FP64 DMMA 8x8x4 tiles, FP64 output       */
+    MM_TF32 = 1,   /* reserved: TF32 operands, FP32 accumulation/output       */
+    MM_TF32X3 = 2  /* reserved: split-TF32 (3 products), FP32 output           */
+} mm_precision;
+
+typedef struct {
+    int32_t n[3];    /* global cells = nodes per axis; n[a] >= 2*order+1        */
+    double h[3];     /* spacing Delta x^mu > 0; domain [0, n*h)                  */
+    int32_t x_begin; /* this rank owns cells/nodes ix in [x_begin, x_end)        */
+    int32_t x_end;   /* single GPU: 0, n[0]  (x_end - x_begin >= order if slab)  */
+} mm_grid;
+
+typedef struct {
+    double qom;   /* q_s/m_s             */
+    double dt;    /* Delta t; beta_s = qom*dt/2             */
+    double c;     /* speed of light, > 0 (normalised units: 1)   */
+    double sigma; /* constant prefactor of eq_mass_matrix_general */
+} mm_species;
+
+typedef struct mm_sorted mm_sorted; /* opaque, library-owned device storage */
+
+typedef struct {
+    int64_t np;        /* particles sorted                                        */
+    int64_t np_padded; /* sorted slots incl. K-padding = seg_begin[nbins]         */
+    int64_t nbins;     /* support-window bins (R12)                     */
+    int64_t capacity;  /* allocated record slots (>= np + nbins*(k_pad-1))        */
+    int32_t order;     /* 1 | 2                                                   */
+    int32_t k_pad;     /* K tile the bins are padded to (multiple of 4)           */
+    int32_t has_B;     /* 0: scalar-only handle (sorted without B)                */
+    int32_t reserved;
+    const int32_t *perm;      /* device [np_padded]: original index, -1 = pad     */
+    const int32_t *seg_begin; /* device [nbins+1]: padded exclusive scan          */
+    const int32_t *seg_count; /* device [nbins]: particles per bin                */
+    const double *rec;        /* device [np_padded][8]: {xi_x,xi_y,xi_z,q,Bx,By,Bz,0} */
+} mm_sorted_info;
+
+/*
+ * mm_sort_by_cell — bin particles by their support window and pad the bins.
+ *
+ * PAPER.md:228 ("particles have been sorted by cell"), PAPER.md:242 (the last
+ * batch of K_t particles is zero-padded) and PAPER.md:285-296
+ * (eq_group_partition: particles grouped by identical support).  The bin of a
+ * particle is its support-window base node j + b (b = 0 for CIC,
+ * b_mu = -1 if xi_mu < 1/2 else 0 for TSC); axis 0 is
+ * unwrapped and local: bx = c_x + b_x - x_begin + order - 1, nbins =
+ * (x_end - x_begin + order - 1) * n1 * n2  (R12).  The sort is
+ * STABLE (ties keep input order), so the permutation is unique and equals
+ * the oracle's bit for bit.
+ *
+ *   g      host, grid/slab geometry
+ *   order  1 | 2;  k_pad: multiple of 4 (4 or 8 typical)
+ *   np     number of particles (0 allowed); must be < 2^31
+ *   pos    device, [np][3] FP64 positions, row-major
+ *   q      device, [np] FP64 charges
+ *   B      device, [np][3] FP64 magnetic field at the particle, or NULL
+ *          (scalar-only handle)
+ *   stream cudaStream_t as void*
+ *   inout  host, address of a handle pointer.  If *inout == NULL a new
+ *          handle is created; otherwise the handle is reused (its device
+ *          buffers grow if needed) and must have been created for the same
+ *          grid and order.  On any error *inout is left unchanged.
+ *
+ * Ownership: the handle owns a sorted, padded copy of the particle data, so
+ * the caller may free pos/q/B after the call.  Release with mm_free().
+ * Synchronisation: the call enqueues its kernels on `stream` and then waits
+ * for that stream once, to read back the error flags (MM_ERR_DOMAIN for a
+ * particle whose cell is outside [x_begin,x_end) x [0,n1) x [0,n2) — never
+ * clamped; MM_ERR_NONFINITE for NaN/Inf).
+ */
+mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos,
+                          const double *q, const double *B, void *stream, mm_sorted **inout);
+
+/* mm_sorted_view — read-only view of a handle's device arrays (see struct). */
+mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
+
+/*
+ * mm_assemble — the mass matrix of one species from a sorted handle.
+ *
+ * Algorithm 1: for each support-window bin (= support
+ * group), batches of K_t = 4 particles build A^{ij} = W s^{ij} and B = W^T
+ * (eq_AB_batch) and accumulate D^{ij} += A^{ij} B on FP64 DMMA 8x8x4 tiles
+ * (eq_mma_accumulate); the finished tiles are scattered into the node-stencil
+ * storage.  Order 2 pads the 27-node support to 32 and
+ * computes the 10 upper 8x8 tiles (spatial symmetry, eq_spatial_symmetry).
+ *
+ *   h          sorted handle (mm_sort_by_cell) for the same grid
+ *   kind       MM_SCALAR | MM_TENSOR (MM_TENSOR needs a handle sorted with B)
+ *   prec       MM_FP64 (MM_TF32/MM_TF32X3 return MM_ERR_INCOMPATIBLE in this
+ *              version)
+ *   sp         host, species constants (qom, dt, c > 0, sigma)
+ *   accumulate 0: out = M (the owned rows are overwritten);
+ *              1: out += M (species sum)
+ *   out        device, FP64 [(x_end-x_begin)*n1*n2][S][C] (layout above)
+ *   ghost      device, FP64 [mm_ghost_planes(order)][n1*n2][S][C], required
+ *              when the grid is a slab (x_begin > 0 or x_end < n[0]) and
+ *              ignored (may be NULL) otherwise.  Rows of nodes outside the
+ *              slab are added here: order 1 -> plane 0 = node plane x_end;
+ *              order 2 -> planes 0,1,2 = x_begin-1, x_end, x_end+1.  It is
+ *              zeroed first unless accumulate = 1.
+ *   stream     cudaStream_t as void*
+ * Fully asynchronous.  The handle must not be re-sorted or freed until the
+ * stream has passed this call.
+ */
+mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp,
+                      int accumulate, double *out, double *ghost, void *stream);
+
+/*
+ * mm_ghost_add — add `nplanes` received ghost node planes into owned rows
+ * (the reduction step of the slab decomposition):
+ *   out[((first_plane + k)*n1*n2 + r)*S*C + e] += recv[(k*n1*n2 + r)*S*C + e]
+ * for k < nplanes.  `first_plane` is relative to x_begin.  Asynchronous.
+ */
+mm_status mm_ghost_add(const mm_grid *g, int order, mm_kind kind, double *out, const double *recv,
+                       int first_plane, int nplanes, void *stream);
+
+/* Number of ghost node planes of a slab: 1 (order 1) or 3 (order 2). */
+int mm_ghost_planes(int order);
+
+/* Elements (doubles) of the owned output: (x_end-x_begin)*n1*n2*S*C, or -1. */
+int64_t mm_out_elems(const mm_grid *g, int order, mm_kind kind);
+
+/* Release a handle (NULL is a no-op).  Synchronises the device first. */
+void mm_free(mm_sorted *h);
+
+/* Thread-local description of the last failure of this thread (host string). */
+const char *mm_last_error(void);
+
+/* Library version string, e.g. "mm-b200 0.1 sm_100a". */
+const char *mm_version(void);
+
+/* Number of kernel launches this library has issued since load (host counter,
+ * used by the benchmark's gpu_launches claim). */
+int64_t mm_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MM_H_ */

@@ -1,0 +1,384 @@
+// C ABI of libmm (include/mm.h): argument validation, handle lifetime, stream
+// plumbing and error strings.  All arithmetic lives in the kernels of
+// mm_sort.cu, mm_assemble_fp64.cu and mm_halo.cu.
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "mm_internal.cuh"
+
+struct mm_sorted {
+    mm_grid g;
+    int order;
+    int k_pad;
+    int has_B;
+    int valid;
+    int device;
+    int64_t np, np_padded, nbins;
+    int64_t cap_np;   // particle-indexed arrays
+    int64_t cap_rec;  // record slots
+    uint32_t *key;
+    int32_t *rank;
+    int32_t *count;
+    int32_t *seg_begin;
+    int32_t *perm;
+    double *rec;
+    int32_t *scan_tmp;
+    int32_t *mid_list;
+    int32_t *huge_list;
+    int32_t *d_status;
+    int32_t *h_status;  // pinned
+};
+
+namespace {
+
+thread_local std::string g_err;
+std::atomic<int64_t> g_launches{0};
+
+mm_status fail(mm_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+mm_status cuda_fail(cudaError_t e, const char *where)
+{
+    if (e == cudaErrorMemoryAllocation)
+        return fail(MM_ERR_OUT_OF_MEMORY, "%s: %s", where, cudaGetErrorString(e));
+    return fail(MM_ERR_CUDA, "%s: %s", where, cudaGetErrorString(e));
+}
+
+mm_status check_grid(const mm_grid *g, int order)
+{
+    if (!g)
+        return fail(MM_ERR_INVALID_ARG, "grid is NULL");
+    if (order != 1 && order != 2)
+        return fail(MM_ERR_INVALID_ARG, "order must be 1 or 2 (got %d)", order);
+    for (int a = 0; a < 3; ++a) {
+        if (g->n[a] < 2 * order + 1)
+            return fail(MM_ERR_INVALID_ARG, "n[%d] = %d < 2*order+1 (stencil offsets would alias)", a, g->n[a]);
+        if (!(g->h[a] > 0.0) || !std::isfinite(g->h[a]))
+            return fail(MM_ERR_INVALID_ARG, "h[%d] must be finite and > 0", a);
+    }
+    if (g->x_begin < 0 || g->x_end > g->n[0] || g->x_end <= g->x_begin)
+        return fail(MM_ERR_INVALID_ARG, "bad slab [%d, %d) for n[0] = %d", g->x_begin, g->x_end, g->n[0]);
+    const bool whole = g->x_begin == 0 && g->x_end == g->n[0];
+    if (!whole && g->x_end - g->x_begin < order)
+        return fail(MM_ERR_INVALID_ARG, "slab width %d < order %d", g->x_end - g->x_begin, order);
+    int64_t nbins = (int64_t)(g->x_end - g->x_begin + order - 1) * g->n[1] * g->n[2];
+    if (nbins >= INT32_MAX)
+        return fail(MM_ERR_INVALID_ARG, "too many bins (%lld)", (long long)nbins);
+    return MM_OK;
+}
+
+void release(mm_sorted *h)
+{
+    if (!h)
+        return;
+    cudaFree(h->key);
+    cudaFree(h->rank);
+    cudaFree(h->count);
+    cudaFree(h->seg_begin);
+    cudaFree(h->perm);
+    cudaFree(h->rec);
+    cudaFree(h->scan_tmp);
+    cudaFree(h->mid_list);
+    cudaFree(h->huge_list);
+    cudaFree(h->d_status);
+    if (h->h_status)
+        cudaFreeHost(h->h_status);
+    delete h;
+}
+
+}  // namespace
+
+namespace mm {
+
+void count_launch(int n)
+{
+    g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+
+Geo make_geo(const mm_grid &g, int order)
+{
+    Geo o;
+    o.n0 = g.n[0];
+    o.n1 = g.n[1];
+    o.n2 = g.n[2];
+    o.h0 = g.h[0];
+    o.h1 = g.h[1];
+    o.h2 = g.h[2];
+    o.x_begin = g.x_begin;
+    o.x_end = g.x_end;
+    o.order = order;
+    o.periodic_x = (g.x_begin == 0 && g.x_end == g.n[0]) ? 1 : 0;
+    o.nbx = g.x_end - g.x_begin + order - 1;
+    return o;
+}
+
+}  // namespace mm
+
+extern "C" {
+
+const char *mm_last_error(void)
+{
+    return g_err.c_str();
+}
+
+const char *mm_version(void)
+{
+    return "mm-b200 0.1 sm_100a (FP64 DMMA 8x8x4)";
+}
+
+int64_t mm_launch_count(void)
+{
+    return g_launches.load();
+}
+
+int mm_ghost_planes(int order)
+{
+    return order == 1 ? 1 : (order == 2 ? 3 : -1);
+}
+
+int64_t mm_out_elems(const mm_grid *g, int order, mm_kind kind)
+{
+    if (check_grid(g, order) != MM_OK || (kind != MM_SCALAR && kind != MM_TENSOR))
+        return -1;
+    int64_t S = (2 * order + 1) * (2 * order + 1) * (2 * order + 1);
+    return (int64_t)(g->x_end - g->x_begin) * g->n[1] * g->n[2] * S * (int64_t)kind;
+}
+
+mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos, const double *q,
+                          const double *B, void *stream, mm_sorted **inout)
+{
+    try {
+        mm_status st = check_grid(g, order);
+        if (st)
+            return st;
+        if (!inout)
+            return fail(MM_ERR_INVALID_ARG, "inout is NULL");
+        if (k_pad < 4 || k_pad % 4 != 0 || k_pad > 1024)
+            return fail(MM_ERR_INVALID_ARG, "k_pad must be a positive multiple of 4 (got %d)", k_pad);
+        if (np < 0 || np >= INT32_MAX)
+            return fail(MM_ERR_INVALID_ARG, "np out of range (%lld)", (long long)np);
+        if (np > 0 && (!pos || !q))
+            return fail(MM_ERR_INVALID_ARG, "pos/q must not be NULL");
+        const int64_t nbins = (int64_t)(g->x_end - g->x_begin + order - 1) * g->n[1] * g->n[2];
+        const int64_t cap_rec = np + nbins * (k_pad - 1);
+        if (cap_rec >= INT32_MAX)
+            return fail(MM_ERR_INVALID_ARG, "np + nbins*(k_pad-1) exceeds 2^31");
+        mm_sorted *h = *inout;
+        const bool fresh = (h == nullptr);
+        if (!fresh) {
+            if (h->order != order || memcmp(h->g.n, g->n, sizeof(g->n)) || h->g.x_begin != g->x_begin ||
+                h->g.x_end != g->x_end || memcmp(h->g.h, g->h, sizeof(g->h)))
+                return fail(MM_ERR_INCOMPATIBLE, "handle was created for another grid/order");
+        } else {
+            h = new (std::nothrow) mm_sorted;
+            if (!h)
+                return fail(MM_ERR_OUT_OF_MEMORY, "host allocation failed");
+            memset(h, 0, sizeof(*h));
+            h->g = *g;
+            h->order = order;
+            cudaGetDevice(&h->device);
+        }
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaError_t e = cudaSuccess;
+        if (np > h->cap_np || !h->key) {
+            cudaFree(h->key);
+            cudaFree(h->rank);
+            h->key = nullptr;
+            h->rank = nullptr;
+            h->cap_np = 0;
+            const size_t n = (size_t)(np > 0 ? np : 1);
+            e = cudaMalloc((void **)&h->key, sizeof(uint32_t) * n);
+            if (!e) e = cudaMalloc((void **)&h->rank, sizeof(int32_t) * n);
+            if (!e) h->cap_np = (int64_t)n;
+        }
+        if (!e && (cap_rec > h->cap_rec || !h->perm)) {
+            cudaFree(h->perm);
+            cudaFree(h->rec);
+            h->perm = nullptr;
+            h->rec = nullptr;
+            h->cap_rec = 0;
+            const size_t n = (size_t)(cap_rec > 0 ? cap_rec : 1);
+            e = cudaMalloc((void **)&h->perm, sizeof(int32_t) * n);
+            if (!e) e = cudaMalloc((void **)&h->rec, sizeof(double) * 8 * n);
+            if (!e) h->cap_rec = (int64_t)n;
+        }
+        if (!e && !h->count) {
+            const size_t nb = (size_t)(nbins > 0 ? nbins : 1);
+            e = cudaMalloc((void **)&h->count, sizeof(int32_t) * nb);
+            if (!e) e = cudaMalloc((void **)&h->seg_begin, sizeof(int32_t) * (nb + 1));
+            if (!e) e = cudaMalloc((void **)&h->mid_list, sizeof(int32_t) * nb);
+            if (!e) e = cudaMalloc((void **)&h->huge_list, sizeof(int32_t) * nb);
+            if (!e) e = cudaMalloc((void **)&h->scan_tmp, sizeof(int32_t) * (size_t)mm::scan_tmp_elems(nbins));
+            if (!e) e = cudaMalloc((void **)&h->d_status, sizeof(int32_t) * mm::ST_WORDS);
+            if (!e) e = cudaMallocHost((void **)&h->h_status, sizeof(int32_t) * mm::ST_WORDS);
+        }
+        if (e) {
+            if (fresh)
+                release(h);
+            return cuda_fail(e, "mm_sort_by_cell allocation");
+        }
+        h->k_pad = k_pad;
+        h->has_B = B ? 1 : 0;
+        h->nbins = nbins;
+        h->np = np;
+        h->valid = 0;
+        mm::SortBufs b;
+        b.np = np;
+        b.nbins = nbins;
+        b.k_pad = k_pad;
+        b.pos = pos;
+        b.q = q;
+        b.B = B;
+        b.key = h->key;
+        b.rank = h->rank;
+        b.count = h->count;
+        b.seg_begin = h->seg_begin;
+        b.perm = h->perm;
+        b.rec = h->rec;
+        b.scan_tmp = h->scan_tmp;
+        b.mid_list = h->mid_list;
+        b.huge_list = h->huge_list;
+        b.status = h->d_status;
+        b.capacity = h->cap_rec;
+        e = mm::sort_enqueue(mm::make_geo(*g, order), b, s);
+        if (!e)
+            e = cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int32_t) * mm::ST_WORDS, cudaMemcpyDeviceToHost, s);
+        if (!e)
+            e = cudaStreamSynchronize(s);
+        if (e) {
+            if (fresh)
+                release(h);
+            return cuda_fail(e, "mm_sort_by_cell");
+        }
+        const int err = h->h_status[mm::ST_ERR];
+        if (err) {
+            if (fresh)
+                release(h);
+            if (err & mm::ERR_NONFINITE)
+                return fail(MM_ERR_NONFINITE, "NaN/Inf in particle positions, charges or B");
+            return fail(MM_ERR_DOMAIN, "particle outside the owned cell slab [%d,%d)x[0,%d)x[0,%d)", g->x_begin,
+                        g->x_end, g->n[1], g->n[2]);
+        }
+        h->np_padded = h->h_status[mm::ST_NPAD];
+        h->valid = 1;
+        *inout = h;
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_sort_by_cell");
+    }
+}
+
+mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)
+{
+    if (!h || !out)
+        return fail(MM_ERR_INVALID_ARG, "NULL argument");
+    if (!h->valid)
+        return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
+    out->np = h->np;
+    out->np_padded = h->np_padded;
+    out->nbins = h->nbins;
+    out->capacity = h->cap_rec;
+    out->order = h->order;
+    out->k_pad = h->k_pad;
+    out->has_B = h->has_B;
+    out->reserved = 0;
+    out->perm = h->perm;
+    out->seg_begin = h->seg_begin;
+    out->seg_count = h->count;
+    out->rec = h->rec;
+    return MM_OK;
+}
+
+mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, int accumulate,
+                      double *out, double *ghost, void *stream)
+{
+    try {
+        if (!h || !sp || !out)
+            return fail(MM_ERR_INVALID_ARG, "NULL handle, species or out");
+        if (!h->valid)
+            return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
+        if (kind != MM_SCALAR && kind != MM_TENSOR)
+            return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
+        if (prec != MM_FP64)
+            return fail(MM_ERR_INCOMPATIBLE, "precision %d not available in this build (MM_FP64 only)", (int)prec);
+        if (kind == MM_TENSOR && !h->has_B)
+            return fail(MM_ERR_INCOMPATIBLE, "MM_TENSOR needs a handle sorted with B");
+        if (!(sp->c > 0.0) || !std::isfinite(sp->qom) || !std::isfinite(sp->dt) || !std::isfinite(sp->sigma) ||
+            !std::isfinite(sp->c))
+            return fail(MM_ERR_INVALID_ARG, "species constants must be finite with c > 0");
+        mm::Geo geo = mm::make_geo(h->g, h->order);
+        if (!geo.periodic_x && !ghost)
+            return fail(MM_ERR_INVALID_ARG, "slab grid needs a ghost buffer");
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t S = (2 * h->order + 1) * (2 * h->order + 1) * (2 * h->order + 1);
+        const int64_t rowlen = S * (int64_t)kind;
+        const int64_t nout = (int64_t)(h->g.x_end - h->g.x_begin) * h->g.n[1] * h->g.n[2] * rowlen;
+        const int64_t nghost = geo.periodic_x ? 0 : (int64_t)mm_ghost_planes(h->order) * h->g.n[1] * h->g.n[2] * rowlen;
+        cudaError_t e = cudaSuccess;
+        if (!accumulate) {
+            e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nout, s);
+            if (!e && nghost)
+                e = cudaMemsetAsync(ghost, 0, sizeof(double) * (size_t)nghost, s);
+            if (e)
+                return cuda_fail(e, "mm_assemble memset");
+        }
+        mm::AsmArgs a;
+        a.rec = h->rec;
+        a.seg_begin = h->seg_begin;
+        a.nbins = h->nbins;
+        a.ncomp = (int)kind;
+        a.wscale = sp->qom * sp->dt / 2.0 / sp->c;
+        a.sigma = sp->sigma;
+        a.out = out;
+        a.ghost = geo.periodic_x ? nullptr : ghost;
+        e = mm::assemble_fp64_enqueue(geo, a, s);
+        if (e)
+            return cuda_fail(e, "mm_assemble launch");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_assemble");
+    }
+}
+
+mm_status mm_ghost_add(const mm_grid *g, int order, mm_kind kind, double *out, const double *recv, int first_plane,
+                       int nplanes, void *stream)
+{
+    mm_status st = check_grid(g, order);
+    if (st)
+        return st;
+    if (kind != MM_SCALAR && kind != MM_TENSOR)
+        return fail(MM_ERR_INVALID_ARG, "bad kind");
+    const int w = g->x_end - g->x_begin;
+    if (!out || !recv || nplanes < 0 || first_plane < 0 || first_plane + nplanes > w)
+        return fail(MM_ERR_INVALID_ARG, "bad ghost_add arguments (planes [%d,%d) of %d)", first_plane,
+                    first_plane + nplanes, w);
+    const int64_t S = (2 * order + 1) * (2 * order + 1) * (2 * order + 1);
+    const int64_t plane = (int64_t)g->n[1] * g->n[2] * S * (int64_t)kind;
+    cudaError_t e = mm::ghost_add_enqueue(out + first_plane * plane, recv, nplanes * plane, (cudaStream_t)stream);
+    if (e)
+        return cuda_fail(e, "mm_ghost_add");
+    return MM_OK;
+}
+
+void mm_free(mm_sorted *h)
+{
+    if (!h)
+        return;
+    cudaDeviceSynchronize();
+    release(h);
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// Internal declarations of libmm (not part of the ABI).  See include/mm.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mm.h"
+
+namespace mm {
+
+// Kernel-side grid/slab geometry.
+struct Geo {
+    int n0, n1, n2;
+    double h0, h1, h2;
+    int x_begin, x_end;
+    int order;
+    int periodic_x;  // whole axis 0 owned -> wrap, else slab with ghost planes
+    int nbx;         // bins along axis 0 = x_end - x_begin + order - 1
+};
+
+Geo make_geo(const mm_grid &g, int order);
+
+// Status words in device memory (read back once per sort).
+enum { ST_ERR = 0, ST_NPAD = 1, ST_NMID = 2, ST_NHUGE = 3, ST_WORDS = 8 };
+enum { ERR_DOMAIN = 1, ERR_NONFINITE = 2 };
+
+// Bins larger than these go to the CTA / huge fix-up paths.
+constexpr int WARP_BIN_MAX = 1024;
+constexpr int CTA_BIN_MAX = 16384;
+
+void count_launch(int n = 1);
+
+// ---- sort (mm_sort.cu) ---------------------------------------------------
+struct SortBufs {
+    int64_t np, nbins;
+    int k_pad;
+    const double *pos, *q, *B;
+    uint32_t *key;
+    int32_t *rank;       // atomic rank, later reused as dest (inverse permutation)
+    int32_t *count;      // [nbins]
+    int32_t *seg_begin;  // [nbins + 1]
+    int32_t *perm;       // [capacity]
+    double *rec;         // [capacity][8]
+    int32_t *scan_tmp;   // [>= nblocks + 1]
+    int32_t *mid_list;   // [nbins]
+    int32_t *huge_list;  // [nbins]
+    int32_t *status;     // [ST_WORDS]
+    int64_t capacity;
+};
+int64_t scan_tmp_elems(int64_t nbins);
+cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s);
+
+// ---- assembly (mm_assemble_fp64.cu) ----------------------------------------
+struct AsmArgs {
+    const double *rec;
+    const int32_t *seg_begin;
+    int64_t nbins;
+    int ncomp;            // 1 | 9
+    double wscale;        // omega = wscale * B   (= qom*dt/(2c))
+    double sigma;
+    double *out;          // owned rows
+    double *ghost;        // ghost planes (slab only)
+};
+cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
+
+// ---- halo (mm_halo.cu) -----------------------------------------------------
+cudaError_t ghost_add_enqueue(double *out, const double *recv, int64_t n, cudaStream_t s);
+
+}  // namespace mm

@@ -1,0 +1,170 @@
+// Microbenchmarks that set the roofline denominators this build reports
+// (DESIGN.md §Roofline): FP64 DMMA 8x8x4 and DFMA peaks, global FP64 RED
+// throughput for the deposit pattern, HBM copy.  Not part of the hot path;
+// built as libmm_probe.so.  Each entry point returns the kernel time in ms
+// measured with CUDA events (<0 on error).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace {
+
+__device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
+{
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int CH>
+__global__ void k_dmma(int iters, double *sink, double seed)
+{
+    double acc[CH][2];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        acc[c][0] = acc[c][1] = 0.0;
+    double a = seed * (threadIdx.x + 1), b = seed + threadIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            dmma(acc[c][0], acc[c][1], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        s += acc[c][0] + acc[c][1];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
+template <int CH>
+__global__ void k_dfma(int iters, double *sink, double seed)
+{
+    double acc[CH];
+    double a = seed * (threadIdx.x + 1), b = seed + threadIdx.x;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        acc[c] = c;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            acc[c] = fma(acc[c], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        s += acc[c];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
+// DMMA with interleaved DFMAs (ratio per DMMA) — do they share a pipe?
+template <int CH, int NF>
+__global__ void k_mixed(int iters, double *sink, double seed)
+{
+    double acc[CH][2], f[NF];
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll
+    for (int c = 0; c < NF; ++c)
+        f[c] = c;
+    double a = seed * (threadIdx.x + 1), b = seed + threadIdx.x;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            dmma(acc[c][0], acc[c][1], a, b);
+#pragma unroll
+        for (int c = 0; c < NF; ++c)
+            f[c] = fma(f[c], a, b);
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < CH; ++c)
+        s += acc[c][0] + acc[c][1];
+#pragma unroll
+    for (int c = 0; c < NF; ++c)
+        s += f[c];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
+// Global FP64 reductions: each warp issues `per_warp` rounds; round r of warp w
+// targets a pseudo-random 256-B aligned line (contig=1: 32 lanes -> 32
+// consecutive doubles, i.e. 8 sectors) or a random double per lane (contig=0).
+__global__ void k_red(double *buf, int64_t nelem, int per_warp, int contig, uint32_t seed)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    uint32_t x = (uint32_t)(warp * 2654435761u) ^ seed;
+    for (int r = 0; r < per_warp; ++r) {
+        x = x * 1664525u + 1013904223u;
+        uint32_t y = contig ? x : (x ^ (lane * 0x9E3779B9u)) * 2246822519u;
+        int64_t base = contig ? ((int64_t)(y % (uint32_t)(nelem / 32)) * 32 + lane)
+                              : (int64_t)(y % (uint32_t)nelem);
+        atomicAdd(buf + base, 1.0);
+    }
+}
+
+__global__ void k_copy(const double4 *__restrict__ a, double4 *__restrict__ b, int64_t n)
+{
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+        b[i] = a[i];
+}
+
+template <typename F>
+float timed(F f)
+{
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    f();  // warm-up
+    cudaEventRecord(e0);
+    f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = -1.f;
+    if (cudaGetLastError() == cudaSuccess)
+        cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+// FP64 flops = blocks * threads/32 * iters * 8 chains * 512
+float probe_dmma(int blocks, int threads, int iters, double *sink)
+{
+    return timed([&] { k_dmma<8><<<blocks, threads>>>(iters, sink, 1.0000001); });
+}
+
+// FP64 flops = blocks * threads * iters * 8 chains * 2
+float probe_dfma(int blocks, int threads, int iters, double *sink)
+{
+    return timed([&] { k_dfma<8><<<blocks, threads>>>(iters, sink, 1.0000001); });
+}
+
+// 8 DMMA + 8 DFMA (per lane) per iteration
+float probe_mixed(int blocks, int threads, int iters, double *sink)
+{
+    return timed([&] { k_mixed<8, 8><<<blocks, threads>>>(iters, sink, 1.0000001); });
+}
+
+// REDs = blocks * threads * per_warp
+float probe_red(double *buf, int64_t nelem, int blocks, int threads, int per_warp, int contig)
+{
+    return timed([&] { k_red<<<blocks, threads>>>(buf, nelem, per_warp, contig, 12345u); });
+}
+
+// bytes = 2 * n4 * 32
+float probe_copy(const double *a, double *b, int64_t n4)
+{
+    return timed([&] {
+        k_copy<<<148 * 8, 256>>>(reinterpret_cast<const double4 *>(a), reinterpret_cast<double4 *>(b), n4);
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,86 @@
+"""Multi-rank host logic of the slab decomposition on CPU (gloo, world size 2 and 3).
+
+Each rank takes its own particles (particles owned by cell), computes its owned rows and
+ghost planes (here from the oracle restricted to its particles, standing in for the
+device kernel), runs the real exchange (slab.exchange_ghosts over torch.distributed) and
+the result must equal the whole-domain oracle of all particles."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+from paper_2604_19286_b200 import slab
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, order, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.Config("t", n, order, "tensor", 5, seed=21)
+        widths = [slab.slab_bounds(n[0], world, r)[1] - slab.slab_bounds(n[0], world, r)[0] for r in range(world)]
+        xb, xe = slab.slab_bounds(n[0], world, rank)
+        d = synth.particles(cfg, xb, xe)
+        loc = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])          # whole-domain rows of MY particles
+        plane = n[1] * n[2]
+        S = (2 * order + 1) ** 3
+        loc = loc.reshape(n[0], plane * S * 9)
+        owned = torch.from_numpy(loc[xb:xe].copy())
+        gplanes = [xe % n[0]] if order == 1 else [(xb - 1) % n[0], xe % n[0], (xe + 1) % n[0]]
+        ghost = torch.from_numpy(loc[gplanes].copy())
+        # rows outside owned+ghost planes must be empty (particles owned by cell)
+        others = [x for x in range(n[0]) if not (xb <= x < xe) and x not in gplanes]
+        assert not loc[others].any()
+
+        def add(k, src):
+            owned[k] += src
+
+        slab.exchange_ghosts(owned, ghost, order, plane * S * 9, rank, world, widths, add=add)
+        q.put((rank, xb, xe, owned.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("order", [1, 2])
+def test_slab_exchange_gloo(world, order):
+    n = (12, 5, 6) if world == 2 else (11, 5, 5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, order, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cfg = synth.Config("t", n, order, "tensor", 5, seed=21)
+    d = synth.particles(cfg)
+    ref = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"]).reshape(n[0], -1)
+    for rank, xb, xe, owned in res:
+        scale = np.abs(ref[xb:xe]).max()
+        assert np.abs(owned - ref[xb:xe]).max() <= 1e-13 * scale, rank
+
+
+def test_slab_bounds_cover():
+    for n0 in (5, 12, 64, 257):
+        for w in (1, 2, 3, 8):
+            if n0 < 2 * w:
+                continue
+            b = [slab.slab_bounds(n0, w, r) for r in range(w)]
+            assert b[0][0] == 0 and b[-1][1] == n0
+            assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
