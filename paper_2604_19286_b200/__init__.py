@@ -167,7 +167,7 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
 
 class _CudaArray:
     def __init__(self, ptr, shape, typestr):
-        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr or 0), True),
+        self.__cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (int(ptr or 0), False),
                                          "version": 3, "strides": None}
 
 

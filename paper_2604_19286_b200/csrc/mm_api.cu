@@ -117,6 +117,9 @@ Geo make_geo(const mm_grid &g, int order)
     o.h0 = g.h[0];
     o.h1 = g.h[1];
     o.h2 = g.h[2];
+    o.ih0 = 1.0 / g.h[0];
+    o.ih1 = 1.0 / g.h[1];
+    o.ih2 = 1.0 / g.h[2];
     o.x_begin = g.x_begin;
     o.x_end = g.x_end;
     o.order = order;
@@ -314,7 +317,7 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
             return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
         if (prec != MM_FP64)
             return fail(MM_ERR_INCOMPATIBLE, "precision %d not available in this build (MM_FP64 only)", (int)prec);
-        if (kind == MM_TENSOR && !h->has_B)
+        if (kind == MM_TENSOR && !h->has_B && h->np > 0)
             return fail(MM_ERR_INCOMPATIBLE, "MM_TENSOR needs a handle sorted with B");
         if (!(sp->c > 0.0) || !std::isfinite(sp->qom) || !std::isfinite(sp->dt) || !std::isfinite(sp->sigma) ||
             !std::isfinite(sp->c))

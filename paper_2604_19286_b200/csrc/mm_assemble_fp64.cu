@@ -10,12 +10,19 @@
 //
 // Fragment mapping of mma.sync.m8n8k4.f64 (row.col): lane t holds
 // A[t>>2][t&3], B[t&3][t>>2] and D[t>>2][2(t&3)+v].  With rows = support
-// nodes and k = particles, lane t needs exactly ONE weight, w = W_{t>>2}(p_{t&3}):
-// it is its B element unscaled and, times s^{ij}, its A element.
+// nodes and k = particles, lane t needs exactly ONE weight per 8-node block,
+// w = W_{t>>2}(p_{t&3}): it is its B element unscaled and, times s^{ij}, its
+// A element.
 //
-// Per-particle work (alpha, s, W) is done once per particle by one lane on a
-// chunk of particles read with coalesced 16-B loads and staged in shared
-// memory; the batch loop then reads w and s from shared memory.
+// Structure of both kernels (one warp = one bin [x component group]):
+//   prep    one lane per particle of a chunk: 2 x 256-bit record loads, s^{ij}
+//           (alpha, eq_alpha_matrix) and the tensor-product weights W_a,
+//           staged in shared memory in bank-conflict-free layouts;
+//   batch   per batch of 4 particles: LDS of w and s, one DMUL per A element,
+//           one DMMA per tile and component (accumulators in registers);
+//   deposit D staged in shared memory, then FP64 REDs driven by a per-lane
+//           table (node index, slot offset) and node-row pointers broadcast by
+//           warp shuffles, issued in address order (contiguous runs).
 #include "mm_internal.cuh"
 
 namespace mm {
@@ -29,9 +36,26 @@ __device__ __forceinline__ void dmma(double &d0, double &d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+// 256-bit read-only record load (LDG.E.ENL2.256 on sm_100a).
+__device__ __forceinline__ double4 ld256(const double *p)
+{
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ int wrapi(int i, int n)
 {
     return i < 0 ? i + n : (i >= n ? i - n : i);
+}
+
+__device__ __forceinline__ double *shfl_ptr(double *p, int src)
+{
+    unsigned long long v = (unsigned long long)p;
+    unsigned lo = __shfl_sync(0xffffffffu, (unsigned)v, src), hi = __shfl_sync(0xffffffffu, (unsigned)(v >> 32), src);
+    return (double *)(((unsigned long long)hi << 32) | lo);
 }
 
 // Base address of node row (X unwrapped global, Y/Z wrapped); rowlen = S*C.
@@ -77,27 +101,34 @@ __device__ __forceinline__ void coeff(double q, double Bx, double By, double Bz,
 // w_k = phi(xi - (b + k)).
 __device__ __forceinline__ void weights1(double xi, double w[2])
 {
-    w[0] = 1.0 - xi;                     // phi1(xi)
-    w[1] = 1.0 - fabs(xi - 1.0);         // phi1(xi - 1)
+    w[0] = 1.0 - xi;              // phi1(xi)
+    w[1] = 1.0 - fabs(xi - 1.0);  // phi1(xi - 1)
 }
 
 __device__ __forceinline__ void weights2(double xi, double w[3])
 {
-    double b = xi >= 0.5 ? 0.0 : -1.0;   // R4: tie -> base 0
+    double b = xi >= 0.5 ? 0.0 : -1.0;  // R4: tie -> base 0
     double t0 = fabs(xi - b), t1 = xi - (b + 1.0), t2 = fabs(xi - (b + 2.0));
-    w[0] = 0.5 * (1.5 - t0) * (1.5 - t0);    // 1/2 < |t0| <= 3/2
-    w[1] = 0.75 - t1 * t1;                   // |t1| <= 1/2
-    w[2] = 0.5 * (1.5 - t2) * (1.5 - t2);    // 1/2 <= |t2| <= 3/2
+    w[0] = 0.5 * (1.5 - t0) * (1.5 - t0);  // 1/2 < |t0| <= 3/2
+    w[1] = 0.75 - t1 * t1;                 // |t1| <= 1/2
+    w[2] = 0.5 * (1.5 - t2) * (1.5 - t2);  // 1/2 <= |t2| <= 3/2
 }
 
 constexpr int WARPS = 8;
 
 // ---------------------------------------------------------------- order 1
+// Shared memory per warp (doubles):
+//   sh_w [8 nodes][WS]  node-major, WS = 36: batch reads hit 2 wavefronts (minimum)
+//   sh_s [32][SS]       SS = 10 (even -> 16-B aligned pairs for LDS.128)
+//   stage [8][8][NC]    deposit staging (aliases the above)
 template <int NC>
-struct O1Smem {
-    static constexpr int PREP = 32 * (NC + 8);
+struct O1 {
+    static constexpr int WS = 36;
+    static constexpr int SS = NC == 9 ? 10 : 2;
+    static constexpr int PREP = 8 * WS + 32 * SS;
     static constexpr int STAGE = 64 * NC;
     static constexpr int SIZE = PREP > STAGE ? PREP : STAGE;
+    static constexpr int NDEP = 64 * NC / 32;  // deposit elements per lane
 };
 
 template <int NC>
@@ -106,14 +137,25 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
                                                        double wscale, double sigma, double *__restrict__ out,
                                                        double *__restrict__ ghost)
 {
-    __shared__ __align__(16) double smem[WARPS][O1Smem<NC>::SIZE];
+    using L = O1<NC>;
+    __shared__ __align__(16) double smem[WARPS][L::SIZE];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *sm = smem[warp];
-    double *sh_s = sm;             // [32][NC]
-    double *sh_w = sm + 32 * NC;   // [32][8]
+    double *sh_w = sm;
+    double *sh_s = sm + 8 * L::WS;
     const int64_t nwarps = (int64_t)gridDim.x * WARPS;
     const int plane = g.n1 * g.n2;
     constexpr int RL = 27 * NC;
+
+    // deposit table (per CTA): element e of D[a][b][c] in address order ->
+    // node a (3 bits) | offset (slot*NC + c) within node a's row
+    __shared__ int32_t s_tab[64 * NC];
+    for (int e = threadIdx.x; e < 64 * NC; e += blockDim.x) {
+        const int a = e / (8 * NC), rr = e - a * 8 * NC, b = rr / NC, c = rr - b * NC;
+        const int slot = ((b >> 2) - (a >> 2) + 1) * 9 + (((b >> 1) & 1) - ((a >> 1) & 1) + 1) * 3 + ((b & 1) - (a & 1) + 1);
+        s_tab[e] = a | ((slot * NC + c) << 3);
+    }
+    __syncthreads();
 
     for (int64_t bin = (int64_t)blockIdx.x * WARPS + warp; bin < nbins; bin += nwarps) {
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
@@ -127,56 +169,75 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
         for (int base = b0; base < b1; base += 32) {
             const int m = min(32, b1 - base);
             if (lane < m) {
-                const double2 *r = reinterpret_cast<const double2 *>(rec + 8 * (int64_t)(base + lane));
-                double2 r0 = __ldg(r), r1 = __ldg(r + 1);
+                const double *r = rec + 8 * (int64_t)(base + lane);
+                const double4 r0 = ld256(r);  // xi_x, xi_y, xi_z, q
                 double s[NC];
                 if (NC == 9) {
-                    double2 r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-                    coeff<NC>(r1.y, r2.x, r2.y, r3.x, wscale, sigma, s);
+                    const double4 r1 = ld256(r + 4);  // Bx, By, Bz, 0
+                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
                 } else {
-                    coeff<NC>(r1.y, 0, 0, 0, wscale, sigma, s);
+                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, s);
                 }
                 double wx[2], wy[2], wz[2];
                 weights1(r0.x, wx);
                 weights1(r0.y, wy);
-                weights1(r1.x, wz);
+                weights1(r0.z, wz);
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
-                    sh_s[lane * NC + c] = s[c];
+                    sh_s[lane * L::SS + c] = s[c];
 #pragma unroll
                 for (int a = 0; a < 8; ++a)
-                    sh_w[lane * 8 + a] = wx[a >> 2] * wy[(a >> 1) & 1] * wz[a & 1];
+                    sh_w[a * L::WS + lane] = (wx[a >> 2] * wy[(a >> 1) & 1]) * wz[a & 1];
             }
             __syncwarp();
-            for (int kb = 0; kb < m; kb += 4) {
-                const int p = kb + (lane & 3);
-                const double w = sh_w[p * 8 + (lane >> 2)];
+            const double *wrow = sh_w + (lane >> 2) * L::WS + (lane & 3);
+            const double *srow = sh_s + (lane & 3) * L::SS;
+            auto batch = [&](int kb) {
+                const double w = wrow[kb];
+                const double *sp = srow + kb * L::SS;
+                if (NC == 9) {
 #pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    dmma(acc[c][0], acc[c][1], sh_s[p * NC + c] * w, w);
+                    for (int c = 0; c < 8; c += 2) {
+                        const double2 sv = *reinterpret_cast<const double2 *>(sp + c);
+                        dmma(acc[c][0], acc[c][1], sv.x * w, w);
+                        dmma(acc[c + 1][0], acc[c + 1][1], sv.y * w, w);
+                    }
+                    dmma(acc[NC - 1][0], acc[NC - 1][1], sp[8] * w, w);
+                } else {
+                    dmma(acc[0][0], acc[0][1], sp[0] * w, w);
+                }
+            };
+            if (m == 32) {
+#pragma unroll
+                for (int kb = 0; kb < 32; kb += 4)
+                    batch(kb);
+            } else {
+                for (int kb = 0; kb < m; kb += 4)
+                    batch(kb);
             }
             __syncwarp();
         }
 
-        // ---- deposit: stage D[a][b][c] in shared memory, then RED in address order
+        // ---- deposit: stage D[a][b][c], then RED in address order via the table
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
             sm[(lane >> 2) * 8 * NC + (2 * (lane & 3)) * NC + c] = acc[c][0];
             sm[(lane >> 2) * 8 * NC + (2 * (lane & 3) + 1) * NC + c] = acc[c][1];
         }
-        __syncwarp();
+        // row pointers of the 8 support nodes: lane a < 8 computes node a's
         const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
         const int by = rem / g.n2, bz = rem - by * g.n2;
-        const int X0 = g.x_begin + bx;  // order 1: window base = cell
-        for (int e = lane; e < 64 * NC; e += 32) {
-            const int a = e / (8 * NC), rr = e - a * 8 * NC, b = rr / NC, c = rr - b * NC;
-            const double v = sm[e];
-            if (v != 0.0) {
-                const int ax = a >> 2, ay = (a >> 1) & 1, az = a & 1;
-                const int slot = ((b >> 2) - ax + 1) * 9 + (((b >> 1) & 1) - ay + 1) * 3 + ((b & 1) - az + 1);
-                double *row = row_ptr(g, X0 + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2), out, ghost, RL);
-                atomicAdd(row + slot * NC + c, v);
-            }
+        const int a8 = lane & 7;
+        double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
+                                wrapi(bz + (a8 & 1), g.n2), out, ghost, RL);
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < L::NDEP; ++i) {
+            const double v = sm[i * 32 + lane];
+            const int t = s_tab[i * 32 + lane];
+            double *row = shfl_ptr(myrow, t & 7);
+            if (v != 0.0)
+                atomicAdd(row + (t >> 3), v);
         }
         __syncwarp();
     }
@@ -185,131 +246,177 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
 // ---------------------------------------------------------------- order 2
 // 27-node support padded to 32 = 4 row blocks of 8; the 10 upper 8x8 tiles
 // (r <= c) per component (spatial symmetry, eq_spatial_symmetry); the lower
-// tiles are deposited as mirrors.  A warp owns CG of the NC components of one bin.
-__constant__ int8_t kTileR[10] = {0, 0, 0, 0, 1, 1, 1, 2, 2, 3};
-__constant__ int8_t kTileC[10] = {0, 1, 2, 3, 1, 2, 3, 2, 3, 3};
+// tiles follow by mirroring.  One GROUP of NC warps assembles one bin, warp c
+// owning component c (tensor: the CTA = 9 warps; scalar: a single warp, 8
+// groups per CTA).  The group shares the per-particle prep through shared
+// memory, accumulates its tiles in registers, mirrors them into a full
+// 27 x 27 x NC stage in shared memory and flushes the stage with REDs in
+// global address order: runs of 3 z-adjacent slots x NC components are
+// contiguous in the [g][slot][comp] layout (27*8 B for the tensor).
+template <int NC>
+struct O2 {
+    static constexpr int WPG = NC;                   // warps per group
+    static constexpr int GPC = NC == 9 ? 1 : 4;      // groups per CTA
+    static constexpr int THREADS = WPG * GPC * 32;
+    static constexpr int CH = 32;                    // particles per prep chunk
+    static constexpr int WS = 36;                    // sh_w row stride (doubles)
+    static constexpr int SS = NC;                    // sh_s row stride
+    static constexpr int PREP = 32 * WS + CH * SS + CH * 9;
+    static constexpr int STAGE = 729 * NC;
+    static constexpr int GROUP_DOUBLES = PREP + STAGE + 32;  // + 27 row pointers
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 729 * 2;
+};
 
-template <int NC, int CG>
-__global__ void __launch_bounds__(WARPS * 32) k_asm_o2(Geo g, const double *__restrict__ rec,
-                                                       const int32_t *__restrict__ seg_begin, int64_t nbins,
-                                                       double wscale, double sigma, double *__restrict__ out,
-                                                       double *__restrict__ ghost)
+__device__ __forceinline__ void group_sync(int nthreads, int id)
 {
-    constexpr int NG = NC / CG;
-    constexpr int CH = 16;  // particles staged per chunk
-    constexpr int SM = CH * (32 + CG) > 640 ? CH * (32 + CG) : 640;
-    __shared__ __align__(16) double smem[WARPS][SM];
+    if (nthreads == 32)
+        __syncwarp();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <int NC>
+__global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo g, const double *__restrict__ rec,
+                                                            const int32_t *__restrict__ seg_begin, int64_t nbins,
+                                                            double wscale, double sigma, double *__restrict__ out,
+                                                            double *__restrict__ ghost)
+{
+    using L = O2<NC>;
+    extern __shared__ __align__(16) double dsm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double *sh_w = smem[warp];            // [CH][32]
-    double *sh_s = smem[warp] + CH * 32;  // [CH][CG]
-    const int64_t nwarps = (int64_t)gridDim.x * WARPS;
+    const int grp = warp / L::WPG, comp = warp - grp * L::WPG;
+    const int gtid = threadIdx.x - grp * L::WPG * 32;  // thread index inside the group
+    constexpr int GT = L::WPG * 32;                     // threads per group
+    double *gsm = dsm + grp * L::GROUP_DOUBLES;
+    double *sh_w = gsm;                     // [32 nodes][WS]
+    double *sh_s = sh_w + 32 * L::WS;       // [CH][NC]
+    double *sh_a = sh_s + L::CH * L::SS;    // [CH][9] per-axis weights
+    double *stage = sh_a + L::CH * 9;       // [27][27][NC]
+    double **rowp = reinterpret_cast<double **>(stage + L::STAGE);  // [27]
+    int16_t *s_slot = reinterpret_cast<int16_t *>(dsm + L::GPC * L::GROUP_DOUBLES);  // [27][27]
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * NC;
-    const int64_t nitems = nbins * NG;
 
-    for (int64_t item = (int64_t)blockIdx.x * WARPS + warp; item < nitems; item += nwarps) {
-        const int64_t bin = item / NG;
-        const int grp = (int)(item - bin * NG);
+    for (int e = threadIdx.x; e < 729; e += blockDim.x) {
+        const int a = e / 27, b = e - 27 * a;
+        s_slot[e] = (int16_t)((b / 9 - a / 9 + 2) * 25 + ((b / 3) % 3 - (a / 3) % 3 + 2) * 5 + (b % 3 - a % 3 + 2));
+    }
+    __syncthreads();
+
+    const int64_t ngroups = (int64_t)gridDim.x * L::GPC;
+    for (int64_t bin = (int64_t)blockIdx.x * L::GPC + grp; bin < nbins; bin += ngroups) {
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
         if (b0 == b1)
             continue;
-        double acc[CG][10][2];
+        double acc[10][2];
 #pragma unroll
-        for (int c = 0; c < CG; ++c)
-#pragma unroll
-            for (int t = 0; t < 10; ++t)
-                acc[c][t][0] = acc[c][t][1] = 0.0;
+        for (int t = 0; t < 10; ++t)
+            acc[t][0] = acc[t][1] = 0.0;
 
-        for (int base = b0; base < b1; base += CH) {
-            const int m = min(CH, b1 - base);
-            if (lane < m) {
-                const double2 *r = reinterpret_cast<const double2 *>(rec + 8 * (int64_t)(base + lane));
-                double2 r0 = __ldg(r), r1 = __ldg(r + 1);
+        for (int base = b0; base < b1; base += L::CH) {
+            const int m = min(L::CH, b1 - base);
+            // prep 1: one thread per particle -> s (all components) and per-axis weights
+            if (gtid < m) {
+                const double *r = rec + 8 * (int64_t)(base + gtid);
+                const double4 r0 = ld256(r);
                 double s[NC];
                 if (NC == 9) {
-                    double2 r2 = __ldg(r + 2), r3 = __ldg(r + 3);
-                    coeff<NC>(r1.y, r2.x, r2.y, r3.x, wscale, sigma, s);
+                    const double4 r1 = ld256(r + 4);
+                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
                 } else {
-                    coeff<NC>(r1.y, 0, 0, 0, wscale, sigma, s);
+                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, s);
                 }
-                double wx[3], wy[3], wz[3];
-                weights2(r0.x, wx);
-                weights2(r0.y, wy);
-                weights2(r1.x, wz);
 #pragma unroll
-                for (int c = 0; c < CG; ++c)
-                    sh_s[lane * CG + c] = s[grp * CG + c];
-#pragma unroll
-                for (int a = 0; a < 27; ++a)
-                    sh_w[lane * 32 + a] = wx[a / 9] * wy[(a / 3) % 3] * wz[a % 3];
-#pragma unroll
-                for (int a = 27; a < 32; ++a)
-                    sh_w[lane * 32 + a] = 0.0;
+                for (int c = 0; c < NC; ++c)
+                    sh_s[gtid * L::SS + c] = s[c];
+                double w3[3];
+                weights2(r0.x, w3);
+                sh_a[gtid * 9 + 0] = w3[0]; sh_a[gtid * 9 + 1] = w3[1]; sh_a[gtid * 9 + 2] = w3[2];
+                weights2(r0.y, w3);
+                sh_a[gtid * 9 + 3] = w3[0]; sh_a[gtid * 9 + 4] = w3[1]; sh_a[gtid * 9 + 5] = w3[2];
+                weights2(r0.z, w3);
+                sh_a[gtid * 9 + 6] = w3[0]; sh_a[gtid * 9 + 7] = w3[1]; sh_a[gtid * 9 + 8] = w3[2];
             }
-            __syncwarp();
-            for (int kb = 0; kb < m; kb += 4) {
-                const int p = kb + (lane & 3);
+            group_sync(GT, 1 + grp);
+            // prep 2: tensor-product weights W[a][p] = (wx*wy)*wz, rows 27..31 zero
+            for (int e = gtid; e < 32 * L::CH; e += GT) {
+                const int a = e / L::CH, p = e - a * L::CH;
+                double w = 0.0;
+                if (a < 27 && p < m) {
+                    const double *wa = sh_a + p * 9;
+                    w = (wa[a / 9] * wa[3 + (a / 3) % 3]) * wa[6 + a % 3];
+                }
+                sh_w[a * L::WS + p] = w;
+            }
+            group_sync(GT, 1 + grp);
+            const double *wcol = sh_w + (lane >> 2) * L::WS + (lane & 3);
+            const double *scol = sh_s + (lane & 3) * L::SS + comp;
+            auto batch = [&](int kb) {
                 double w[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
-                    w[r] = sh_w[p * 32 + 8 * r + (lane >> 2)];
+                    w[r] = wcol[8 * r * L::WS + kb];
+                const double s = scol[kb * L::SS];
+                double A[4];
 #pragma unroll
-                for (int c = 0; c < CG; ++c) {
-                    const double s = sh_s[p * CG + c];
-                    double A[4];
-#pragma unroll
-                    for (int r = 0; r < 4; ++r)
-                        A[r] = s * w[r];
-                    dmma(acc[c][0][0], acc[c][0][1], A[0], w[0]);
-                    dmma(acc[c][1][0], acc[c][1][1], A[0], w[1]);
-                    dmma(acc[c][2][0], acc[c][2][1], A[0], w[2]);
-                    dmma(acc[c][3][0], acc[c][3][1], A[0], w[3]);
-                    dmma(acc[c][4][0], acc[c][4][1], A[1], w[1]);
-                    dmma(acc[c][5][0], acc[c][5][1], A[1], w[2]);
-                    dmma(acc[c][6][0], acc[c][6][1], A[1], w[3]);
-                    dmma(acc[c][7][0], acc[c][7][1], A[2], w[2]);
-                    dmma(acc[c][8][0], acc[c][8][1], A[2], w[3]);
-                    dmma(acc[c][9][0], acc[c][9][1], A[3], w[3]);
-                }
+                for (int r = 0; r < 4; ++r)
+                    A[r] = s * w[r];
+                dmma(acc[0][0], acc[0][1], A[0], w[0]);
+                dmma(acc[1][0], acc[1][1], A[0], w[1]);
+                dmma(acc[2][0], acc[2][1], A[0], w[2]);
+                dmma(acc[3][0], acc[3][1], A[0], w[3]);
+                dmma(acc[4][0], acc[4][1], A[1], w[1]);
+                dmma(acc[5][0], acc[5][1], A[1], w[2]);
+                dmma(acc[6][0], acc[6][1], A[1], w[3]);
+                dmma(acc[7][0], acc[7][1], A[2], w[2]);
+                dmma(acc[8][0], acc[8][1], A[2], w[3]);
+                dmma(acc[9][0], acc[9][1], A[3], w[3]);
+            };
+            if (m == L::CH) {
+#pragma unroll 2
+                for (int kb = 0; kb < L::CH; kb += 4)
+                    batch(kb);
+            } else {
+                for (int kb = 0; kb < m; kb += 4)
+                    batch(kb);
             }
-            __syncwarp();
+            group_sync(GT, 1 + grp);
         }
 
-        // ---- deposit: per component, stage the 10 tiles in shared memory, then
-        //      RED each valid entry (a, b < 27) and, off the diagonal tiles, its mirror.
+        // ---- stage the full 27x27 block of component `comp` (mirror of the upper tiles)
         const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
         const int by = rem / g.n2, bz = rem - by * g.n2;
-        const int X0 = g.x_begin + bx - 1;  // window base node along axis 0
-        double *stage = smem[warp];
+        if (gtid < 27) {
+            const int a = gtid;
+            rowp[a] = row_ptr(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
+                              wrapi(bz + a % 3, g.n2), out, ghost, RL);
+        }
 #pragma unroll
-        for (int c = 0; c < CG; ++c) {
-            __syncwarp();
+        for (int t = 0; t < 10; ++t) {
+            const int tr = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
+            const int tc = t < 4 ? t : (t < 7 ? t - 3 : (t < 9 ? t - 5 : 3));
+            const int a = 8 * tr + (lane >> 2);
 #pragma unroll
-            for (int t = 0; t < 10; ++t) {
-                stage[t * 64 + (lane >> 2) * 8 + 2 * (lane & 3)] = acc[c][t][0];
-                stage[t * 64 + (lane >> 2) * 8 + 2 * (lane & 3) + 1] = acc[c][t][1];
-            }
-            __syncwarp();
-            const int comp = grp * CG + c;
-#pragma unroll 1
-            for (int e = lane; e < 640; e += 32) {
-                const int t = e >> 6, tr = kTileR[t], tc = kTileC[t];
-                const int a = 8 * tr + ((e >> 3) & 7), b = 8 * tc + (e & 7);
-                if (a >= 27 || b >= 27)
-                    continue;
-                const double v = stage[e];
-                const int ax = a / 9, ay = (a / 3) % 3, az = a % 3;
-                const int bxx = b / 9, byy = (b / 3) % 3, bzz = b % 3;
-                const int sab = (bxx - ax + 2) * 25 + (byy - ay + 2) * 5 + (bzz - az + 2);
-                double *ra = row_ptr(g, X0 + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2), out, ghost, RL);
-                atomicAdd(ra + sab * NC + comp, v);
-                if (tr != tc) {
-                    double *rb = row_ptr(g, X0 + bxx, wrapi(by + byy, g.n1), wrapi(bz + bzz, g.n2), out, ghost, RL);
-                    atomicAdd(rb + (124 - sab) * NC + comp, v);  // slot(-d) = S-1-slot(d)
+            for (int v = 0; v < 2; ++v) {
+                const int b = 8 * tc + 2 * (lane & 3) + v;
+                if (a < 27 && b < 27) {
+                    stage[(a * 27 + b) * NC + comp] = acc[t][v];
+                    if (tr != tc)
+                        stage[(b * 27 + a) * NC + comp] = acc[t][v];
                 }
             }
         }
-        __syncwarp();
+        group_sync(GT, 1 + grp);
+        // ---- flush in address order: e = (a*27 + b)*NC + c -> row(a) + slot(b - a)*NC + c
+        for (int e = gtid; e < 729 * NC; e += GT) {
+            const int ab = NC == 1 ? e : e / NC;
+            const int c = e - ab * NC;
+            const int a = ab / 27;
+            const double v = stage[e];
+            if (v != 0.0)
+                atomicAdd(rowp[a] + s_slot[ab] * NC + c, v);
+        }
+        group_sync(GT, 1 + grp);
     }
 }
 
@@ -328,6 +435,30 @@ unsigned grid_for(K kernel, int64_t items)
     return (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
 }
 
+template <int NC>
+cudaError_t launch_o2(const Geo &geo, const AsmArgs &a, cudaStream_t s)
+{
+    using L = O2<NC>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_asm_o2<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        if (e)
+            return e;
+        attr = true;
+    }
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o2<NC>, L::THREADS, L::SMEM);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (a.nbins + L::GPC - 1) / L::GPC;
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+    k_asm_o2<NC><<<grid, L::THREADS, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
+                                                   a.ghost);
+    count_launch();
+    return cudaGetLastError();
+}
+
 }  // namespace
 
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s)
@@ -343,13 +474,9 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
                 geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost);
         }
     } else {
-        if (a.ncomp == 9) {
-            k_asm_o2<9, 3><<<grid_for(k_asm_o2<9, 3>, a.nbins * 3), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost);
-        } else {
-            k_asm_o2<1, 1><<<grid_for(k_asm_o2<1, 1>, a.nbins), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost);
-        }
+        if (a.ncomp == 9)
+            return launch_o2<9>(geo, a, s);
+        return launch_o2<1>(geo, a, s);
     }
     count_launch();
     return cudaGetLastError();

@@ -12,6 +12,7 @@ namespace mm {
 struct Geo {
     int n0, n1, n2;
     double h0, h1, h2;
+    double ih0, ih1, ih2;  // RN(1/h): Markstein-corrected division in locate (R5)
     int x_begin, x_end;
     int order;
     int periodic_x;  // whole axis 0 owned -> wrap, else slab with ghost planes

@@ -40,6 +40,7 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
     L.err = 0;
     const double x[3] = {x0, x1, x2};
     const double h[3] = {g.h0, g.h1, g.h2};
+    const double ih[3] = {g.ih0, g.ih1, g.ih2};
 #pragma unroll
     for (int mu = 0; mu < 3; ++mu) {
         if (!isfinite(x[mu])) {
@@ -48,7 +49,11 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
             L.c[mu] = 0;
             continue;
         }
-        double u = __ddiv_rn(x[mu], h[mu]);
+        // u = RN(x/h) via Markstein's correction: with y = RN(1/h) and q0 = RN(x*y) within
+        // 1 ulp of x/h, r = x - h*q0 is exact (FMA) and RN(q0 + r*y) = RN(x/h).
+        const double q0 = x[mu] * ih[mu];
+        const double r = fma(-q0, h[mu], x[mu]);
+        double u = fma(r, ih[mu], q0);
         double c = floor(u);
         L.xi[mu] = u - c;
         double lo = mu == 0 ? (double)g.x_begin : 0.0;
@@ -63,25 +68,35 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
     return L;
 }
 
-__global__ void k_key(Geo g, int64_t np, const double *__restrict__ pos, const double *__restrict__ q,
-                      const double *__restrict__ B, uint32_t *__restrict__ key,
-                      int32_t *__restrict__ rank, int32_t *__restrict__ count,
-                      int32_t *__restrict__ status)
+__device__ __forceinline__ double4 ld256(const double *p)
 {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= np)
-        return;
-    Located L = locate(g, pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]);
-    int err = L.err;
-    if (!isfinite(q[p]))
-        err |= ERR_NONFINITE;
-    if (B && !(isfinite(B[3 * p]) && isfinite(B[3 * p + 1]) && isfinite(B[3 * p + 2])))
-        err |= ERR_NONFINITE;
-    if (err) {
-        atomicOr(&status[ST_ERR], err);
-        key[p] = 0xffffffffu;
-        return;
+    double4 v;
+    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v.x), "=d"(v.y), "=d"(v.z), "=d"(v.w)
+                 : "l"(p));
+    return v;
+}
+
+// Load the 3-vectors of particles p0..p0+3 ([np][3] FP64); VEC: three 256-bit loads.
+template <bool VEC>
+__device__ __forceinline__ void load_vec3x4(const double *__restrict__ a, int64_t p0, int64_t np, double v[12])
+{
+    if (VEC && p0 + 4 <= np) {
+        double4 x = ld256(a + 3 * p0), y = ld256(a + 3 * p0 + 4), z = ld256(a + 3 * p0 + 8);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+        v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+                v[3 * j + m] = (p0 + j < np) ? a[3 * (p0 + j) + m] : 0.0;
     }
+}
+
+__device__ __forceinline__ uint32_t bin_of(const Geo &g, const Located &L)
+{
     int32_t b[3];
 #pragma unroll
     for (int mu = 0; mu < 3; ++mu)
@@ -89,9 +104,47 @@ __global__ void k_key(Geo g, int64_t np, const double *__restrict__ pos, const d
     int32_t bx = L.c[0] + b[0] - g.x_begin + (g.order - 1);
     int32_t by = wrapi(L.c[1] + b[1], g.n1);
     int32_t bz = wrapi(L.c[2] + b[2], g.n2);
-    uint32_t k = (uint32_t)(((int64_t)bx * g.n1 + by) * g.n2 + bz);
-    key[p] = k;
-    rank[p] = atomicAdd(&count[k], 1);
+    return (uint32_t)(((int64_t)bx * g.n1 + by) * g.n2 + bz);
+}
+
+// Four particles per thread: more independent loads and atomics in flight.
+template <bool VEC>
+__global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const double *__restrict__ pos, uint32_t *__restrict__ key,
+                      int32_t *__restrict__ rank, int32_t *__restrict__ count, int32_t *__restrict__ status)
+{
+    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (p0 >= np)
+        return;
+    double x[12];
+    load_vec3x4<VEC>(pos, p0, np, x);
+    uint32_t k[4];
+    int err = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        k[j] = 0xffffffffu;
+        if (p0 + j < np) {
+            Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
+            if (L.err)
+                err |= L.err;
+            else
+                k[j] = bin_of(g, L);
+        }
+    }
+    if (err)
+        atomicOr(&status[ST_ERR], err);
+    int r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        r[j] = (k[j] != 0xffffffffu) ? atomicAdd(&count[k[j]], 1) : 0;
+    if (p0 + 4 <= np) {
+        *reinterpret_cast<uint4 *>(key + p0) = make_uint4(k[0], k[1], k[2], k[3]);
+        *reinterpret_cast<int4 *>(rank + p0) = make_int4(r[0], r[1], r[2], r[3]);
+    } else {
+        for (int j = 0; j < 4 && p0 + j < np; ++j) {
+            key[p0 + j] = k[j];
+            rank[p0 + j] = r[j];
+        }
+    }
 }
 
 // ---- K-padded exclusive scan ----------------------------------------------
@@ -199,29 +252,49 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_add(int32_t *__restrict__ seg_b
 __global__ void k_place(int64_t np, const uint32_t *__restrict__ key, const int32_t *__restrict__ rank,
                         const int32_t *__restrict__ seg_begin, int32_t *__restrict__ perm)
 {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= np)
+    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (p0 >= np)
         return;
-    uint32_t k = key[p];
-    if (k == 0xffffffffu)
-        return;
-    perm[seg_begin[k] + rank[p]] = (int32_t)p;
+    uint32_t k[4];
+    int r[4];
+    if (p0 + 4 <= np) {
+        uint4 kk = *reinterpret_cast<const uint4 *>(key + p0);
+        int4 rr = *reinterpret_cast<const int4 *>(rank + p0);
+        k[0] = kk.x; k[1] = kk.y; k[2] = kk.z; k[3] = kk.w;
+        r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            k[j] = p0 + j < np ? key[p0 + j] : 0xffffffffu;
+            r[j] = p0 + j < np ? rank[p0 + j] : 0;
+        }
+    }
+    int sb[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        sb[j] = k[j] != 0xffffffffu ? __ldg(seg_begin + k[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        if (k[j] != 0xffffffffu)
+            perm[sb[j] + r[j]] = (int32_t)(p0 + j);
 }
 
 // ---- per-bin fix-up: ascending order of original indices == stable sort ----
 constexpr int FIX_WARPS = 8;
+
+__device__ __forceinline__ void st256(double *p, double a, double b, double c, double d)
+{
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
 
 __device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int64_t from, int64_t to, int tid,
                                           int nthr)
 {
     for (int64_t i = from + tid; i < to; i += nthr) {
         perm[i] = -1;
-        double2 z = make_double2(0.0, 0.0);
-        double2 *r = reinterpret_cast<double2 *>(rec + 8 * i);
-        r[0] = z;
-        r[1] = z;
-        r[2] = z;
-        r[3] = z;
+        st256(rec + 8 * i, 0.0, 0.0, 0.0, 0.0);
+        st256(rec + 8 * i + 4, 0.0, 0.0, 0.0, 0.0);
     }
 }
 
@@ -251,9 +324,35 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
             }
             continue;
         }
-        if (n == 1) {
-            if (lane == 0)
-                dest[perm[b]] = (int32_t)b;
+        if (n <= 64) {
+            // bitonic sort of 64 keys held as (v0 = elem lane, v1 = elem lane + 32), via shuffles
+            int32_t v0 = lane < n ? perm[b + lane] : INT_MAX;
+            int32_t v1 = lane + 32 < n ? perm[b + lane + 32] : INT_MAX;
+            const int K = n <= 32 ? 32 : 64;
+            for (int k = 2; k <= K; k <<= 1) {
+                for (int j = k >> 1; j > 0; j >>= 1) {
+                    if (j == 32) {
+                        int32_t lo = min(v0, v1), hi = max(v0, v1);
+                        v0 = lo;
+                        v1 = hi;  // k == 64: index lane has (lane & 64) == 0 -> ascending
+                    } else {
+                        const bool lower = (lane & j) == 0;
+                        int32_t p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                        int32_t p1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                        const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
+                        v0 = (lower == up0) ? min(v0, p0) : max(v0, p0);
+                        v1 = (lower == up1) ? min(v1, p1) : max(v1, p1);
+                    }
+                }
+            }
+            if (lane < n) {
+                perm[b + lane] = v0;
+                dest[v0] = (int32_t)(b + lane);
+            }
+            if (lane + 32 < n) {
+                perm[b + lane + 32] = v1;
+                dest[v1] = (int32_t)(b + lane + 32);
+            }
             continue;
         }
         int N = 32;
@@ -356,25 +455,61 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
     }
 }
 
-__global__ void k_scatter(Geo g, int64_t np, const double *__restrict__ pos, const double *__restrict__ q,
+template <bool VEC>
+__global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const double *__restrict__ pos, const double *__restrict__ q,
                           const double *__restrict__ B, const uint32_t *__restrict__ key,
-                          const int32_t *__restrict__ dest, double *__restrict__ rec)
+                          const int32_t *__restrict__ dest, double *__restrict__ rec,
+                          int32_t *__restrict__ status)
 {
-    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (p >= np || key[p] == 0xffffffffu)
+    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (p0 >= np)
         return;
-    Located L = locate(g, pos[3 * p], pos[3 * p + 1], pos[3 * p + 2]);
-    double2 *r = reinterpret_cast<double2 *>(rec + 8 * (int64_t)dest[p]);
-    r[0] = make_double2(L.xi[0], L.xi[1]);
-    if (B) {
-        r[1] = make_double2(L.xi[2], q[p]);
-        r[2] = make_double2(B[3 * p], B[3 * p + 1]);
-        r[3] = make_double2(B[3 * p + 2], 0.0);
+    const bool full = p0 + 4 <= np;
+    uint32_t k[4];
+    int d[4];
+    double qq[4], x[12], bb[12];
+    if (full) {
+        uint4 kk = *reinterpret_cast<const uint4 *>(key + p0);
+        int4 dd = *reinterpret_cast<const int4 *>(dest + p0);
+        k[0] = kk.x; k[1] = kk.y; k[2] = kk.z; k[3] = kk.w;
+        d[0] = dd.x; d[1] = dd.y; d[2] = dd.z; d[3] = dd.w;
     } else {
-        r[1] = make_double2(L.xi[2], q[p]);
-        r[2] = make_double2(0.0, 0.0);
-        r[3] = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            k[j] = p0 + j < np ? key[p0 + j] : 0xffffffffu;
+            d[j] = p0 + j < np ? dest[p0 + j] : 0;
+        }
     }
+    load_vec3x4<VEC>(pos, p0, np, x);
+    if (VEC && full) {
+        double4 t = ld256(q + p0);
+        qq[0] = t.x; qq[1] = t.y; qq[2] = t.z; qq[3] = t.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            qq[j] = p0 + j < np ? q[p0 + j] : 0.0;
+    }
+    if (B) {
+        load_vec3x4<VEC>(B, p0, np, bb);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+            bb[j] = 0.0;
+    }
+    int err = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (k[j] == 0xffffffffu)
+            continue;
+        Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
+        if (!(isfinite(qq[j]) && isfinite(bb[3 * j]) && isfinite(bb[3 * j + 1]) && isfinite(bb[3 * j + 2])))
+            err |= ERR_NONFINITE;
+        double *r = rec + 8 * (int64_t)d[j];
+        st256(r, L.xi[0], L.xi[1], L.xi[2], qq[j]);
+        st256(r + 4, bb[3 * j], bb[3 * j + 1], bb[3 * j + 2], 0.0);
+    }
+    if (err)
+        atomicOr(&status[ST_ERR], err);
 }
 
 inline unsigned blocks_for(int64_t n, int t)
@@ -397,8 +532,12 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     if ((e = cudaMemsetAsync(b.status, 0, sizeof(int32_t) * ST_WORDS, s)))
         return e;
     const int T = 256;
+    const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
     if (b.np > 0) {
-        k_key<<<blocks_for(b.np, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.count, b.status);
+        if (vec)
+            k_key<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
+        else
+            k_key<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
         count_launch();
     }
     const int nblk = (int)((b.nbins + SCAN_TILE - 1) / SCAN_TILE);
@@ -407,7 +546,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
     count_launch(3);
     if (b.np > 0) {
-        k_place<<<blocks_for(b.np, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
+        k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
         count_launch();
     }
     {
@@ -435,7 +574,12 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         count_launch();
     }
     if (b.np > 0) {
-        k_scatter<<<blocks_for(b.np, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.rec);
+        if (vec)
+            k_scatter<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
+                                                                      b.rec, b.status);
+        else
+            k_scatter<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
+                                                                       b.rec, b.status);
         count_launch();
     }
     return cudaGetLastError();

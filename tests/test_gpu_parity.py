@@ -58,6 +58,29 @@ def test_sort_bit_exact(order, k_pad, lattice):
     assert (rec.view(np.uint64) == r["rec"].view(np.uint64)).all()
 
 
+@pytest.mark.parametrize("order", [1, 2])
+def test_sort_bit_exact_nonpow2_spacing(order):
+    # xi = x/h - floor(x/h) must be bit-identical to the oracle's IEEE division for any h
+    # (R5; the kernel uses Markstein's correction of x * RN(1/h))
+    n, h = (7, 9, 6), (0.3, 1.7, 0.77)
+    rng = np.random.default_rng(17 + order)
+    npart = 300000
+    pos = rng.random((npart, 3)) * np.array(n) * np.array(h)
+    # plus positions on and next to nodes
+    k = rng.integers(0, 6, (20000, 3)) * np.array(h)
+    pos[:20000] = np.nextafter(k, k + rng.choice([-1.0, 1.0, 0.0], size=k.shape) * 10) % (np.array(n) * h)
+    pos[20000:40000] = k % (np.array(n) * h)
+    L = np.array(n) * np.array(h)
+    pos = np.where(pos >= L, 0.0, pos)
+    d = {"pos": pos, "q": rng.uniform(-1, 1, npart), "B": rng.uniform(-1, 1, (npart, 3))}
+    _, _, hd = run_gpu(n, order, 9, d, h=h)
+    v = mm().mm_sorted_view(hd)
+    r = oracle.sort(n, order, 4, d["pos"], d["q"], d["B"], h=h)
+    assert (v["perm"].cpu().numpy() == r["perm"]).all()
+    assert (v["seg_begin"].cpu().numpy() == r["seg_begin"]).all()
+    assert (v["rec"].cpu().numpy().view(np.uint64) == r["rec"].view(np.uint64)).all()
+
+
 def test_sort_bit_exact_c2_full():
     cfg = synth.config("c2")
     d = synth.particles(cfg)
