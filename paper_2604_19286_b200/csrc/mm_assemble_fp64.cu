@@ -46,6 +46,14 @@ __device__ __forceinline__ double4 ld256(const double *p)
     return v;
 }
 
+// Fire-and-forget FP64 reduction into GLOBAL memory (REDG.E.ADD.F64.RN).  Explicit PTX:
+// pointers that travel through shuffles/shared memory are generic to the compiler,
+// which would otherwise emit a generic ATOM with a shared-memory CAS fallback.
+__device__ __forceinline__ void red_add(double *p, double v)
+{
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
 __device__ __forceinline__ int wrapi(int i, int n)
 {
     return i < 0 ? i + n : (i >= n ? i - n : i);
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
             const int t = s_tab[i * 32 + lane];
             double *row = shfl_ptr(myrow, t & 7);
             if (v != 0.0)
-                atomicAdd(row + (t >> 3), v);
+                red_add(row + (t >> 3), v);
         }
         __syncwarp();
     }
@@ -414,7 +422,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             const int a = ab / 27;
             const double v = stage[e];
             if (v != 0.0)
-                atomicAdd(rowp[a] + s_slot[ab] * NC + c, v);
+                red_add(rowp[a] + s_slot[ab] * NC + c, v);
         }
         group_sync(GT, 1 + grp);
     }
