@@ -32,6 +32,7 @@ struct mm_sorted {
     int32_t *huge_list;
     int32_t *d_status;
     int32_t *h_status;  // pinned
+    int32_t *d_work;    // assembly work counter
 };
 
 namespace {
@@ -94,6 +95,7 @@ void release(mm_sorted *h)
     cudaFree(h->mid_list);
     cudaFree(h->huge_list);
     cudaFree(h->d_status);
+    cudaFree(h->d_work);
     if (h->h_status)
         cudaFreeHost(h->h_status);
     delete h;
@@ -117,9 +119,6 @@ Geo make_geo(const mm_grid &g, int order)
     o.h0 = g.h[0];
     o.h1 = g.h[1];
     o.h2 = g.h[2];
-    o.ih0 = 1.0 / g.h[0];
-    o.ih1 = 1.0 / g.h[1];
-    o.ih2 = 1.0 / g.h[2];
     o.x_begin = g.x_begin;
     o.x_end = g.x_end;
     o.order = order;
@@ -226,6 +225,7 @@ mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, co
             if (!e) e = cudaMalloc((void **)&h->huge_list, sizeof(int32_t) * nb);
             if (!e) e = cudaMalloc((void **)&h->scan_tmp, sizeof(int32_t) * (size_t)mm::scan_tmp_elems(nbins));
             if (!e) e = cudaMalloc((void **)&h->d_status, sizeof(int32_t) * mm::ST_WORDS);
+            if (!e) e = cudaMalloc((void **)&h->d_work, sizeof(int32_t) * 4);
             if (!e) e = cudaMallocHost((void **)&h->h_status, sizeof(int32_t) * mm::ST_WORDS);
         }
         if (e) {
@@ -338,7 +338,11 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
             if (e)
                 return cuda_fail(e, "mm_assemble memset");
         }
+        e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t), s);
+        if (e)
+            return cuda_fail(e, "mm_assemble memset");
         mm::AsmArgs a;
+        a.work = h->d_work;
         a.rec = h->rec;
         a.seg_begin = h->seg_begin;
         a.nbins = h->nbins;

@@ -143,7 +143,7 @@ template <int NC>
 __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__restrict__ rec,
                                                        const int32_t *__restrict__ seg_begin, int64_t nbins,
                                                        double wscale, double sigma, double *__restrict__ out,
-                                                       double *__restrict__ ghost)
+                                                       double *__restrict__ ghost, int *__restrict__ work)
 {
     using L = O1<NC>;
     __shared__ __align__(16) double smem[WARPS][L::SIZE];
@@ -151,7 +151,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
     double *sm = smem[warp];
     double *sh_w = sm;
     double *sh_s = sm + 8 * L::WS;
-    const int64_t nwarps = (int64_t)gridDim.x * WARPS;
     const int plane = g.n1 * g.n2;
     constexpr int RL = 27 * NC;
 
@@ -165,7 +164,13 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
     }
     __syncthreads();
 
-    for (int64_t bin = (int64_t)blockIdx.x * WARPS + warp; bin < nbins; bin += nwarps) {
+    for (;;) {
+        int nb = 0;
+        if (lane == 0)
+            nb = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
+        const int64_t bin = __shfl_sync(0xffffffffu, nb, 0);
+        if (bin >= nbins)
+            break;
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
         if (b0 == b1)
             continue;
@@ -272,7 +277,7 @@ struct O2 {
     static constexpr int PREP = 32 * WS + CH * SS + CH * 9;
     static constexpr int STAGE = 729 * NC;
     static constexpr int GROUP_DOUBLES = PREP + STAGE + 32;  // + 27 row pointers
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 729 * 2;
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 729 * 2 + 2 + 4 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -287,7 +292,7 @@ template <int NC>
 __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo g, const double *__restrict__ rec,
                                                             const int32_t *__restrict__ seg_begin, int64_t nbins,
                                                             double wscale, double sigma, double *__restrict__ out,
-                                                            double *__restrict__ ghost)
+                                                            double *__restrict__ ghost, int *__restrict__ work)
 {
     using L = O2<NC>;
     extern __shared__ __align__(16) double dsm[];
@@ -311,11 +316,19 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     }
     __syncthreads();
 
-    const int64_t ngroups = (int64_t)gridDim.x * L::GPC;
-    for (int64_t bin = (int64_t)blockIdx.x * L::GPC + grp; bin < nbins; bin += ngroups) {
+    int *s_next = reinterpret_cast<int *>(s_slot + 729) + grp;  // per-group work ticket
+    for (;;) {
+        if (gtid == 0)
+            *s_next = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality)
+        group_sync(GT, 1 + grp);
+        const int64_t bin = *s_next;
+        if (bin >= nbins)
+            break;
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
-        if (b0 == b1)
+        if (b0 == b1) {
+            group_sync(GT, 1 + grp);
             continue;
+        }
         double acc[10][2];
 #pragma unroll
         for (int t = 0; t < 10; ++t)
@@ -323,38 +336,43 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
 
         for (int base = b0; base < b1; base += L::CH) {
             const int m = min(L::CH, b1 - base);
-            // prep 1: one thread per particle -> s (all components) and per-axis weights
-            if (gtid < m) {
-                const double *r = rec + 8 * (int64_t)(base + gtid);
+            // prep 1: one lane per particle; warp 0 -> s (all components), warp 1 (or 0) ->
+            // per-axis weights
+            const int pw = L::WPG > 1 ? 1 : 0;
+            if (comp == 0 && lane < m) {
+                const double *r = rec + 8 * (int64_t)(base + lane);
                 const double4 r0 = ld256(r);
-                double s[NC];
+                double sv[NC];
                 if (NC == 9) {
                     const double4 r1 = ld256(r + 4);
-                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
+                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, sv);
                 } else {
-                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, s);
+                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, sv);
                 }
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
-                    sh_s[gtid * L::SS + c] = s[c];
+                    sh_s[lane * L::SS + c] = sv[c];
+            }
+            if (comp == pw && lane < m) {
+                const double4 r0 = ld256(rec + 8 * (int64_t)(base + lane));
                 double w3[3];
                 weights2(r0.x, w3);
-                sh_a[gtid * 9 + 0] = w3[0]; sh_a[gtid * 9 + 1] = w3[1]; sh_a[gtid * 9 + 2] = w3[2];
+                sh_a[lane * 9 + 0] = w3[0]; sh_a[lane * 9 + 1] = w3[1]; sh_a[lane * 9 + 2] = w3[2];
                 weights2(r0.y, w3);
-                sh_a[gtid * 9 + 3] = w3[0]; sh_a[gtid * 9 + 4] = w3[1]; sh_a[gtid * 9 + 5] = w3[2];
+                sh_a[lane * 9 + 3] = w3[0]; sh_a[lane * 9 + 4] = w3[1]; sh_a[lane * 9 + 5] = w3[2];
                 weights2(r0.z, w3);
-                sh_a[gtid * 9 + 6] = w3[0]; sh_a[gtid * 9 + 7] = w3[1]; sh_a[gtid * 9 + 8] = w3[2];
+                sh_a[lane * 9 + 6] = w3[0]; sh_a[lane * 9 + 7] = w3[1]; sh_a[lane * 9 + 8] = w3[2];
             }
             group_sync(GT, 1 + grp);
-            // prep 2: tensor-product weights W[a][p] = (wx*wy)*wz, rows 27..31 zero
-            for (int e = gtid; e < 32 * L::CH; e += GT) {
-                const int a = e / L::CH, p = e - a * L::CH;
+            // prep 2: tensor-product weights W[a][p] = (wx*wy)*wz (rows 27..31 zero); warp c
+            // owns nodes a = c, c + WPG, ... so the node digits are warp-uniform
+            for (int a = comp; a < 32; a += L::WPG) {
                 double w = 0.0;
-                if (a < 27 && p < m) {
-                    const double *wa = sh_a + p * 9;
+                if (a < 27 && lane < m) {
+                    const double *wa = sh_a + lane * 9;
                     w = (wa[a / 9] * wa[3 + (a / 3) % 3]) * wa[6 + a % 3];
                 }
-                sh_w[a * L::WS + p] = w;
+                sh_w[a * L::WS + lane] = w;
             }
             group_sync(GT, 1 + grp);
             const double *wcol = sh_w + (lane >> 2) * L::WS + (lane & 3);
@@ -415,14 +433,25 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             }
         }
         group_sync(GT, 1 + grp);
-        // ---- flush in address order: e = (a*27 + b)*NC + c -> row(a) + slot(b - a)*NC + c
-        for (int e = gtid; e < 729 * NC; e += GT) {
-            const int ab = NC == 1 ? e : e / NC;
-            const int c = e - ab * NC;
-            const int a = ab / 27;
-            const double v = stage[e];
-            if (v != 0.0)
-                red_add(rowp[a] + s_slot[ab] * NC + c, v);
+        // ---- flush in address order.  Tensor: 243 runs (node a, b_x, b_y) of 27 contiguous
+        //      doubles (b_z = 0..2 x 9 comps) -> row(a) + slot(b0 - a)*9 + lane.
+        if (NC == 9) {
+            for (int run = comp; run < 243; run += L::WPG) {
+                const int a = run / 9, j = run - 9 * a;
+                const int b0 = 9 * (j / 3) + 3 * (j % 3);
+                const int ab0 = a * 27 + b0;
+                if (lane < 27) {
+                    const double v = stage[ab0 * 9 + lane];
+                    if (v != 0.0)
+                        red_add(rowp[a] + s_slot[ab0] * 9 + lane, v);
+                }
+            }
+        } else {
+            for (int e = gtid; e < 729; e += GT) {
+                const double v = stage[e];
+                if (v != 0.0)
+                    red_add(rowp[e / 27] + s_slot[e], v);
+            }
         }
         group_sync(GT, 1 + grp);
     }
@@ -462,7 +491,7 @@ cudaError_t launch_o2(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
     k_asm_o2<NC><<<grid, L::THREADS, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
-                                                   a.ghost);
+                                                   a.ghost, a.work);
     count_launch();
     return cudaGetLastError();
 }
@@ -476,10 +505,10 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
     if (geo.order == 1) {
         if (a.ncomp == 9) {
             k_asm_o1<9><<<grid_for(k_asm_o1<9>, a.nbins), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost);
+                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost, a.work);
         } else {
             k_asm_o1<1><<<grid_for(k_asm_o1<1>, a.nbins), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost);
+                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost, a.work);
         }
     } else {
         if (a.ncomp == 9)

@@ -12,7 +12,6 @@ namespace mm {
 struct Geo {
     int n0, n1, n2;
     double h0, h1, h2;
-    double ih0, ih1, ih2;  // RN(1/h): Markstein-corrected division in locate (R5)
     int x_begin, x_end;
     int order;
     int periodic_x;  // whole axis 0 owned -> wrap, else slab with ghost planes
@@ -61,6 +60,7 @@ struct AsmArgs {
     double sigma;
     double *out;          // owned rows
     double *ghost;        // ghost planes (slab only)
+    int *work;            // device work counter, zeroed before the launch
 };
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
 

@@ -40,7 +40,6 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
     L.err = 0;
     const double x[3] = {x0, x1, x2};
     const double h[3] = {g.h0, g.h1, g.h2};
-    const double ih[3] = {g.ih0, g.ih1, g.ih2};
 #pragma unroll
     for (int mu = 0; mu < 3; ++mu) {
         if (!isfinite(x[mu])) {
@@ -49,11 +48,7 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
             L.c[mu] = 0;
             continue;
         }
-        // u = RN(x/h) via Markstein's correction: with y = RN(1/h) and q0 = RN(x*y) within
-        // 1 ulp of x/h, r = x - h*q0 is exact (FMA) and RN(q0 + r*y) = RN(x/h).
-        const double q0 = x[mu] * ih[mu];
-        const double r = fma(-q0, h[mu], x[mu]);
-        double u = fma(r, ih[mu], q0);
+        double u = __ddiv_rn(x[mu], h[mu]);  // IEEE RN division (bit-exact binning)
         double c = floor(u);
         L.xi[mu] = u - c;
         double lo = mu == 0 ? (double)g.x_begin : 0.0;

@@ -61,7 +61,7 @@ def test_sort_bit_exact(order, k_pad, lattice):
 @pytest.mark.parametrize("order", [1, 2])
 def test_sort_bit_exact_nonpow2_spacing(order):
     # xi = x/h - floor(x/h) must be bit-identical to the oracle's IEEE division for any h
-    # (R5; the kernel uses Markstein's correction of x * RN(1/h))
+    # (R5)
     n, h = (7, 9, 6), (0.3, 1.7, 0.77)
     rng = np.random.default_rng(17 + order)
     npart = 300000
