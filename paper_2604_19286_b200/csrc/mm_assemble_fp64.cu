@@ -277,7 +277,7 @@ struct O2 {
     static constexpr int PREP = 32 * WS + CH * SS + CH * 9;
     static constexpr int STAGE = 729 * NC;
     static constexpr int GROUP_DOUBLES = PREP + STAGE + 32;  // + 27 row pointers
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 729 * 2 + 2 + 4 * GPC;
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 + 4 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     }
     __syncthreads();
 
-    int *s_next = reinterpret_cast<int *>(s_slot + 729) + grp;  // per-group work ticket
+    int *s_next = reinterpret_cast<int *>(s_slot + 730) + grp;  // per-group work ticket (4-B aligned)
     for (;;) {
         if (gtid == 0)
             *s_next = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality)
