@@ -140,7 +140,7 @@ struct O1 {
 };
 
 template <int NC>
-__global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *__restrict__ rec,
                                                        const int32_t *__restrict__ seg_begin, int64_t nbins,
                                                        double wscale, double sigma, double *__restrict__ out,
                                                        double *__restrict__ ghost, int *__restrict__ work)
@@ -164,33 +164,60 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
     }
     __syncthreads();
 
-    for (;;) {
-        int nb = 0;
-        if (lane == 0)
-            nb = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
-        const int64_t bin = __shfl_sync(0xffffffffu, nb, 0);
-        if (bin >= nbins)
-            break;
-        const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
-        if (b0 == b1)
-            continue;
+    // Software pipeline: the next bin's ticket (atomic) and the next chunk's records are
+    // requested one step ahead, so neither latency is exposed at a bin/chunk boundary.
+    int t0 = 0;
+    if (lane == 0)
+        t0 = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
+    int64_t bin = __shfl_sync(0xffffffffu, t0, 0);
+    int tnext = 0;
+    if (lane == 0)
+        tnext = atomicAdd(work, 1);
+    int b0 = 0, b1 = 0;
+    double4 p0 = make_double4(0, 0, 0, 0), p1 = p0;  // prefetched record of this lane
+    if (bin < nbins) {
+        b0 = seg_begin[bin];
+        b1 = seg_begin[bin + 1];
+        if (lane < b1 - b0) {
+            p0 = ld256(rec + 8 * (int64_t)(b0 + lane));
+            if (NC == 9)
+                p1 = ld256(rec + 8 * (int64_t)(b0 + lane) + 4);
+        }
+    }
+    while (bin < nbins) {
         double acc[NC][2];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
             acc[c][0] = acc[c][1] = 0.0;
-
+        int64_t nbin = nbins;
+        int nb0 = 0, nb1 = 0;
         for (int base = b0; base < b1; base += 32) {
             const int m = min(32, b1 - base);
-            if (lane < m) {
-                const double *r = rec + 8 * (int64_t)(base + lane);
-                const double4 r0 = ld256(r);  // xi_x, xi_y, xi_z, q
-                double s[NC];
-                if (NC == 9) {
-                    const double4 r1 = ld256(r + 4);  // Bx, By, Bz, 0
-                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
-                } else {
-                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, s);
+            const double4 r0 = p0, r1 = p1;
+            // prefetch: next chunk of this bin, else the first chunk of the next bin
+            p0 = make_double4(0, 0, 0, 0);
+            p1 = p0;
+            int pf = -1;
+            if (base + 32 < b1) {
+                if (lane < b1 - base - 32)
+                    pf = base + 32 + lane;
+            } else {
+                nbin = __shfl_sync(0xffffffffu, tnext, 0);
+                if (nbin < nbins) {
+                    nb0 = seg_begin[nbin];
+                    nb1 = seg_begin[nbin + 1];
+                    if (lane < nb1 - nb0)
+                        pf = nb0 + lane;
                 }
+            }
+            if (pf >= 0) {
+                p0 = ld256(rec + 8 * (int64_t)pf);
+                if (NC == 9)
+                    p1 = ld256(rec + 8 * (int64_t)pf + 4);
+            }
+            if (lane < m) {
+                double s[NC];
+                coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
                 double wx[2], wy[2], wz[2];
                 weights1(r0.x, wx);
                 weights1(r0.y, wy);
@@ -230,29 +257,46 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
             }
             __syncwarp();
         }
-
-        // ---- deposit: stage D[a][b][c], then RED in address order via the table
+        if (b0 == b1) {  // empty bin: nothing to deposit; fetch the following one
+            nbin = __shfl_sync(0xffffffffu, tnext, 0);
+            if (nbin < nbins) {
+                nb0 = seg_begin[nbin];
+                nb1 = seg_begin[nbin + 1];
+                if (lane < nb1 - nb0) {
+                    p0 = ld256(rec + 8 * (int64_t)(nb0 + lane));
+                    if (NC == 9)
+                        p1 = ld256(rec + 8 * (int64_t)(nb0 + lane) + 4);
+                }
+            }
+        } else {
+            // ---- deposit: stage D[a][b][c], then RED in address order via the table
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-            sm[(lane >> 2) * 8 * NC + (2 * (lane & 3)) * NC + c] = acc[c][0];
-            sm[(lane >> 2) * 8 * NC + (2 * (lane & 3) + 1) * NC + c] = acc[c][1];
-        }
-        // row pointers of the 8 support nodes: lane a < 8 computes node a's
-        const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
-        const int by = rem / g.n2, bz = rem - by * g.n2;
-        const int a8 = lane & 7;
-        double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
-                                wrapi(bz + (a8 & 1), g.n2), out, ghost, RL);
-        __syncwarp();
+            for (int c = 0; c < NC; ++c) {
+                sm[(lane >> 2) * 8 * NC + (2 * (lane & 3)) * NC + c] = acc[c][0];
+                sm[(lane >> 2) * 8 * NC + (2 * (lane & 3) + 1) * NC + c] = acc[c][1];
+            }
+            // row pointers of the 8 support nodes: lane a (mod 8) computes node a's
+            const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+            const int by = rem / g.n2, bz = rem - by * g.n2;
+            const int a8 = lane & 7;
+            double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
+                                    wrapi(bz + (a8 & 1), g.n2), out, ghost, RL);
+            __syncwarp();
 #pragma unroll
-        for (int i = 0; i < L::NDEP; ++i) {
-            const double v = sm[i * 32 + lane];
-            const int t = s_tab[i * 32 + lane];
-            double *row = shfl_ptr(myrow, t & 7);
-            if (v != 0.0)
-                red_add(row + (t >> 3), v);
+            for (int i = 0; i < L::NDEP; ++i) {
+                const double v = sm[i * 32 + lane];
+                const int t = s_tab[i * 32 + lane];
+                double *row = shfl_ptr(myrow, t & 7);
+                if (v != 0.0)
+                    red_add(row + (t >> 3), v);
+            }
+            __syncwarp();
         }
-        __syncwarp();
+        bin = nbin;
+        b0 = nb0;
+        b1 = nb1;
+        if (lane == 0 && bin < nbins)
+            tnext = atomicAdd(work, 1);
     }
 }
 
@@ -260,24 +304,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_asm_o1(Geo g, const double *__re
 // 27-node support padded to 32 = 4 row blocks of 8; the 10 upper 8x8 tiles
 // (r <= c) per component (spatial symmetry, eq_spatial_symmetry); the lower
 // tiles follow by mirroring.  One GROUP of NC warps assembles one bin, warp c
-// owning component c (tensor: the CTA = 9 warps; scalar: a single warp, 8
-// groups per CTA).  The group shares the per-particle prep through shared
-// memory, accumulates its tiles in registers, mirrors them into a full
-// 27 x 27 x NC stage in shared memory and flushes the stage with REDs in
-// global address order: runs of 3 z-adjacent slots x NC components are
-// contiguous in the [g][slot][comp] layout (27*8 B for the tensor).
+// owning component c (tensor: the CTA = 9 warps; scalar: a single warp, GPC
+// groups per CTA).  Each warp preps its own share of the chunk (its lane's
+// particle: s^c and the per-axis weights, then W rows a = c, c+NC, ...) into a
+// double-buffered weight tile, so one group barrier per chunk suffices.  The
+// tiles are mirrored into a full 27 x 27 x NC stage in shared memory and
+// flushed with REDs in global address order: runs of 3 z-adjacent slots x NC
+// components are contiguous in the [g][slot][comp] layout (27*8 B, tensor).
 template <int NC>
 struct O2 {
     static constexpr int WPG = NC;                   // warps per group
     static constexpr int GPC = NC == 9 ? 1 : 4;      // groups per CTA
     static constexpr int THREADS = WPG * GPC * 32;
-    static constexpr int CH = 32;                    // particles per prep chunk
-    static constexpr int WS = 36;                    // sh_w row stride (doubles)
-    static constexpr int SS = NC;                    // sh_s row stride
-    static constexpr int PREP = 32 * WS + CH * SS + CH * 9;
+    static constexpr int CH = 32;                    // particles per chunk
+    static constexpr int WS = 36;                    // weight tile row stride (doubles)
+    static constexpr int WBUF = 32 * WS;             // one weight tile [32 nodes][WS]
     static constexpr int STAGE = 729 * NC;
-    static constexpr int GROUP_DOUBLES = PREP + STAGE + 32;  // + 27 row pointers
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 + 4 * GPC;
+    static constexpr int GROUP_DOUBLES = 2 * WBUF + STAGE + 32;  // + 27 row pointers
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 + 8 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -286,6 +330,26 @@ __device__ __forceinline__ void group_sync(int nthreads, int id)
         __syncwarp();
     else
         asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// s^{c} of one component (c = 3i + j) — eq_alpha_matrix, same expression as coeff<9>.
+__device__ __forceinline__ double coeff_one(int c, double q, double Bx, double By, double Bz, double wscale,
+                                            double sigma)
+{
+    const double o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
+    const double d = 1.0 + (o0 * o0 + o1 * o1 + o2 * o2);
+    const double f = __ddiv_rn(sigma * q, d);
+    switch (c) {
+    case 0: return f * (1.0 + o0 * o0);
+    case 1: return f * (o0 * o1 + o2);
+    case 2: return f * (o0 * o2 - o1);
+    case 3: return f * (o1 * o0 - o2);
+    case 4: return f * (1.0 + o1 * o1);
+    case 5: return f * (o1 * o2 + o0);
+    case 6: return f * (o2 * o0 + o1);
+    case 7: return f * (o2 * o1 - o0);
+    default: return f * (1.0 + o2 * o2);
+    }
 }
 
 template <int NC>
@@ -301,12 +365,11 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     const int gtid = threadIdx.x - grp * L::WPG * 32;  // thread index inside the group
     constexpr int GT = L::WPG * 32;                     // threads per group
     double *gsm = dsm + grp * L::GROUP_DOUBLES;
-    double *sh_w = gsm;                     // [32 nodes][WS]
-    double *sh_s = sh_w + 32 * L::WS;       // [CH][NC]
-    double *sh_a = sh_s + L::CH * L::SS;    // [CH][9] per-axis weights
-    double *stage = sh_a + L::CH * 9;       // [27][27][NC]
+    double *wbuf = gsm;                        // [2][32 nodes][WS]
+    double *stage = gsm + 2 * L::WBUF;         // [27][27][NC]
     double **rowp = reinterpret_cast<double **>(stage + L::STAGE);  // [27]
     int16_t *s_slot = reinterpret_cast<int16_t *>(dsm + L::GPC * L::GROUP_DOUBLES);  // [27][27]
+    int64_t *s_bin = reinterpret_cast<int64_t *>(s_slot + 732) + grp;  // next-bin broadcast (8-B aligned)
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * NC;
 
@@ -314,75 +377,52 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         const int a = e / 27, b = e - 27 * a;
         s_slot[e] = (int16_t)((b / 9 - a / 9 + 2) * 25 + ((b / 3) % 3 - (a / 3) % 3 + 2) * 5 + (b % 3 - a % 3 + 2));
     }
+    // dynamic, in-order bin scheduling; the next ticket is always one bin ahead
+    int tnext = 0;
+    if (gtid == 0) {
+        *s_bin = atomicAdd(work, 1);
+        tnext = atomicAdd(work, 1);
+    }
     __syncthreads();
-
-    int *s_next = reinterpret_cast<int *>(s_slot + 730) + grp;  // per-group work ticket (4-B aligned)
-    for (;;) {
-        if (gtid == 0)
-            *s_next = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality)
-        group_sync(GT, 1 + grp);
-        const int64_t bin = *s_next;
-        if (bin >= nbins)
-            break;
+    int64_t bin = *s_bin;
+    int chunk = 0;  // global chunk counter -> weight buffer parity
+    while (bin < nbins) {
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
-        if (b0 == b1) {
-            group_sync(GT, 1 + grp);
-            continue;
-        }
         double acc[10][2];
 #pragma unroll
         for (int t = 0; t < 10; ++t)
             acc[t][0] = acc[t][1] = 0.0;
-
-        for (int base = b0; base < b1; base += L::CH) {
+        for (int base = b0; base < b1; base += L::CH, ++chunk) {
             const int m = min(L::CH, b1 - base);
-            // prep 1: one lane per particle; warp 0 -> s (all components), warp 1 (or 0) ->
-            // per-axis weights
-            const int pw = L::WPG > 1 ? 1 : 0;
-            if (comp == 0 && lane < m) {
+            double *wt = wbuf + (chunk & 1) * L::WBUF;
+            // prep (every warp, lane = particle): s^comp and this warp's W rows
+            double s_me = 0.0;
+            if (lane < m) {
                 const double *r = rec + 8 * (int64_t)(base + lane);
                 const double4 r0 = ld256(r);
-                double sv[NC];
                 if (NC == 9) {
                     const double4 r1 = ld256(r + 4);
-                    coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, sv);
+                    s_me = coeff_one(comp, r0.w, r1.x, r1.y, r1.z, wscale, sigma);
                 } else {
-                    coeff<NC>(r0.w, 0, 0, 0, wscale, sigma, sv);
+                    s_me = sigma * r0.w;
                 }
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    sh_s[lane * L::SS + c] = sv[c];
-            }
-            if (comp == pw && lane < m) {
-                const double4 r0 = ld256(rec + 8 * (int64_t)(base + lane));
-                double w3[3];
-                weights2(r0.x, w3);
-                sh_a[lane * 9 + 0] = w3[0]; sh_a[lane * 9 + 1] = w3[1]; sh_a[lane * 9 + 2] = w3[2];
-                weights2(r0.y, w3);
-                sh_a[lane * 9 + 3] = w3[0]; sh_a[lane * 9 + 4] = w3[1]; sh_a[lane * 9 + 5] = w3[2];
-                weights2(r0.z, w3);
-                sh_a[lane * 9 + 6] = w3[0]; sh_a[lane * 9 + 7] = w3[1]; sh_a[lane * 9 + 8] = w3[2];
+                double wx[3], wy[3], wz[3];
+                weights2(r0.x, wx);
+                weights2(r0.y, wy);
+                weights2(r0.z, wz);
+                // runtime node digits: select instead of indexing (keeps wx/wy/wz in registers)
+                auto sel = [](const double *w, int i) { return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]); };
+                for (int a = comp; a < 32; a += L::WPG)
+                    wt[a * L::WS + lane] = a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
             }
             group_sync(GT, 1 + grp);
-            // prep 2: tensor-product weights W[a][p] = (wx*wy)*wz (rows 27..31 zero); warp c
-            // owns nodes a = c, c + WPG, ... so the node digits are warp-uniform
-            for (int a = comp; a < 32; a += L::WPG) {
-                double w = 0.0;
-                if (a < 27 && lane < m) {
-                    const double *wa = sh_a + lane * 9;
-                    w = (wa[a / 9] * wa[3 + (a / 3) % 3]) * wa[6 + a % 3];
-                }
-                sh_w[a * L::WS + lane] = w;
-            }
-            group_sync(GT, 1 + grp);
-            const double *wcol = sh_w + (lane >> 2) * L::WS + (lane & 3);
-            const double *scol = sh_s + (lane & 3) * L::SS + comp;
+            const double *wcol = wt + (lane >> 2) * L::WS + (lane & 3);
             auto batch = [&](int kb) {
                 double w[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     w[r] = wcol[8 * r * L::WS + kb];
-                const double s = scol[kb * L::SS];
+                const double s = __shfl_sync(0xffffffffu, s_me, kb + (lane & 3));
                 double A[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
@@ -406,9 +446,18 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                 for (int kb = 0; kb < m; kb += 4)
                     batch(kb);
             }
-            group_sync(GT, 1 + grp);
         }
-
+        if (b0 == b1) {  // empty bin (rare): just advance the ticket
+            if (gtid == 0) {
+                *s_bin = tnext;
+                if (tnext < nbins)
+                    tnext = atomicAdd(work, 1);
+            }
+            group_sync(GT, 1 + grp);
+            bin = *s_bin;
+            group_sync(GT, 1 + grp);
+            continue;
+        }
         // ---- stage the full 27x27 block of component `comp` (mirror of the upper tiles)
         const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
         const int by = rem / g.n2, bz = rem - by * g.n2;
@@ -416,6 +465,11 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             const int a = gtid;
             rowp[a] = row_ptr(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
                               wrapi(bz + a % 3, g.n2), out, ghost, RL);
+        }
+        if (gtid == 0) {
+            *s_bin = tnext;
+            if (tnext < nbins)
+                tnext = atomicAdd(work, 1);
         }
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
@@ -433,13 +487,14 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             }
         }
         group_sync(GT, 1 + grp);
+        bin = *s_bin;
         // ---- flush in address order.  Tensor: 243 runs (node a, b_x, b_y) of 27 contiguous
-        //      doubles (b_z = 0..2 x 9 comps) -> row(a) + slot(b0 - a)*9 + lane.
+        //      doubles (b_z = 0..2 x 9 comps) -> row(a) + slot(b0 - a)*9 + lane.  The next
+        //      write of stage/rowp/s_bin comes after the next chunk barrier.
         if (NC == 9) {
             for (int run = comp; run < 243; run += L::WPG) {
                 const int a = run / 9, j = run - 9 * a;
-                const int b0 = 9 * (j / 3) + 3 * (j % 3);
-                const int ab0 = a * 27 + b0;
+                const int ab0 = a * 27 + 9 * (j / 3) + 3 * (j % 3);
                 if (lane < 27) {
                     const double v = stage[ab0 * 9 + lane];
                     if (v != 0.0)
@@ -453,7 +508,6 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                     red_add(rowp[e / 27] + s_slot[e], v);
             }
         }
-        group_sync(GT, 1 + grp);
     }
 }
 
