@@ -122,6 +122,54 @@ __device__ __forceinline__ void weights2(double xi, double w[3])
     w[2] = 0.5 * (1.5 - t2) * (1.5 - t2);  // 1/2 <= |t2| <= 3/2
 }
 
+// Atomic ticket (inline PTX: keeps the compiler from warp-aggregating it, which would
+// broadcast the result with a shuffle right after the atomic and expose its latency).
+__device__ __forceinline__ int atom_add(int *p, int v)
+{
+    int r;
+    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
+    return r;
+}
+
+// ---- mbarrier + TMA bulk copy (cp.async.bulk) helpers -------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void fence_mbar_init()
+{
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+// One-lane bulk copy global -> shared of `bytes` (multiple of 16), completing on `bar`.
+__device__ __forceinline__ void tma_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
+{
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
 constexpr int WARPS = 8;
 
 // ---------------------------------------------------------------- order 1
@@ -137,16 +185,23 @@ struct O1 {
     static constexpr int STAGE = 64 * NC;
     static constexpr int SIZE = PREP > STAGE ? PREP : STAGE;
     static constexpr int NDEP = 64 * NC / 32;  // deposit elements per lane
+    static constexpr size_t SMEM = (size_t)(WARPS * 2 * 256 + WARPS * SIZE + WARPS * 2) * 8 + 64 * NC * 4;
 };
 
 template <int NC>
 __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *__restrict__ rec,
-                                                       const int32_t *__restrict__ seg_begin, int64_t nbins,
-                                                       double wscale, double sigma, double *__restrict__ out,
-                                                       double *__restrict__ ghost, int *__restrict__ work)
+                                                          const int32_t *__restrict__ seg_begin, int64_t nbins,
+                                                          double wscale, double sigma, double *__restrict__ out,
+                                                          double *__restrict__ ghost, int *__restrict__ work)
 {
     using L = O1<NC>;
-    __shared__ __align__(16) double smem[WARPS][L::SIZE];
+    // dynamic shared memory: [WARPS][2][256] TMA-staged record chunks | [WARPS][SIZE] prep/stage |
+    // [WARPS][2] mbarriers | [64*NC] deposit table
+    extern __shared__ __align__(128) double dsm1[];
+    double(*s_rec)[2][32 * 8] = reinterpret_cast<double(*)[2][32 * 8]>(dsm1);
+    double(*smem)[L::SIZE] = reinterpret_cast<double(*)[L::SIZE]>(dsm1 + WARPS * 2 * 256);
+    uint64_t(*s_bar)[2] = reinterpret_cast<uint64_t(*)[2]>(dsm1 + WARPS * 2 * 256 + WARPS * L::SIZE);
+    int32_t *s_tab = reinterpret_cast<int32_t *>(dsm1 + WARPS * 2 * 256 + WARPS * L::SIZE + WARPS * 2);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *sm = smem[warp];
     double *sh_w = sm;
@@ -156,33 +211,34 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
 
     // deposit table (per CTA): element e of D[a][b][c] in address order ->
     // node a (3 bits) | offset (slot*NC + c) within node a's row
-    __shared__ int32_t s_tab[64 * NC];
     for (int e = threadIdx.x; e < 64 * NC; e += blockDim.x) {
         const int a = e / (8 * NC), rr = e - a * 8 * NC, b = rr / NC, c = rr - b * NC;
         const int slot = ((b >> 2) - (a >> 2) + 1) * 9 + (((b >> 1) & 1) - ((a >> 1) & 1) + 1) * 3 + ((b & 1) - (a & 1) + 1);
         s_tab[e] = a | ((slot * NC + c) << 3);
     }
+    if (lane == 0) {
+        mbar_init(&s_bar[warp][0], 1);
+        mbar_init(&s_bar[warp][1], 1);
+        fence_mbar_init();
+    }
     __syncthreads();
 
-    // Software pipeline: the next bin's ticket (atomic) and the next chunk's records are
-    // requested one step ahead, so neither latency is exposed at a bin/chunk boundary.
-    int t0 = 0;
-    if (lane == 0)
-        t0 = atomicAdd(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
+    // Software pipeline: the next bin's ticket and the next chunk's records (one 2-KB
+    // cp.async.bulk per chunk into a double-buffered shared-memory slot) are requested one
+    // chunk ahead, so neither latency is exposed at a bin/chunk boundary.
+    int t0 = 0, tnext = 0;
+    if (lane == 0) {
+        t0 = atom_add(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
+        tnext = atom_add(work, 1);
+    }
     int64_t bin = __shfl_sync(0xffffffffu, t0, 0);
-    int tnext = 0;
-    if (lane == 0)
-        tnext = atomicAdd(work, 1);
     int b0 = 0, b1 = 0;
-    double4 p0 = make_double4(0, 0, 0, 0), p1 = p0;  // prefetched record of this lane
+    uint32_t buf = 0, phases = 0u;  // bit b: expected parity of buffer b's mbarrier
     if (bin < nbins) {
         b0 = seg_begin[bin];
         b1 = seg_begin[bin + 1];
-        if (lane < b1 - b0) {
-            p0 = ld256(rec + 8 * (int64_t)(b0 + lane));
-            if (NC == 9)
-                p1 = ld256(rec + 8 * (int64_t)(b0 + lane) + 4);
-        }
+        if (lane == 0 && b1 > b0)
+            tma_load(&s_rec[warp][0][0], rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &s_bar[warp][0]);
     }
     while (bin < nbins) {
         double acc[NC][2];
@@ -193,35 +249,42 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
         int nb0 = 0, nb1 = 0;
         for (int base = b0; base < b1; base += 32) {
             const int m = min(32, b1 - base);
-            const double4 r0 = p0, r1 = p1;
-            // prefetch: next chunk of this bin, else the first chunk of the next bin
-            p0 = make_double4(0, 0, 0, 0);
-            p1 = p0;
-            int pf = -1;
+            // prefetch the next chunk of this bin, else the first chunk of the next bin
+            int pf = -1, pfn = 0;
             if (base + 32 < b1) {
-                if (lane < b1 - base - 32)
-                    pf = base + 32 + lane;
+                pf = base + 32;
+                pfn = min(32, b1 - pf);
             } else {
                 nbin = __shfl_sync(0xffffffffu, tnext, 0);
                 if (nbin < nbins) {
                     nb0 = seg_begin[nbin];
                     nb1 = seg_begin[nbin + 1];
-                    if (lane < nb1 - nb0)
-                        pf = nb0 + lane;
+                    if (nb1 > nb0) {
+                        pf = nb0;
+                        pfn = min(32, nb1 - nb0);
+                    }
                 }
             }
-            if (pf >= 0) {
-                p0 = ld256(rec + 8 * (int64_t)pf);
-                if (NC == 9)
-                    p1 = ld256(rec + 8 * (int64_t)pf + 4);
-            }
+            if (lane == 0 && pf >= 0)
+                tma_load(&s_rec[warp][buf ^ 1][0], rec + 8 * (int64_t)pf, pfn * 64, &s_bar[warp][buf ^ 1]);
+            mbar_wait(&s_bar[warp][buf], (phases >> buf) & 1u);
+            phases ^= 1u << buf;
             if (lane < m) {
+                const double *r = &s_rec[warp][buf][8 * lane];
+                const double2 ra = *reinterpret_cast<const double2 *>(r);      // xi_x, xi_y
+                const double2 rb = *reinterpret_cast<const double2 *>(r + 2);  // xi_z, q
                 double s[NC];
-                coeff<NC>(r0.w, r1.x, r1.y, r1.z, wscale, sigma, s);
+                if (NC == 9) {
+                    const double2 rc = *reinterpret_cast<const double2 *>(r + 4);  // Bx, By
+                    const double bz = r[6];
+                    coeff<NC>(rb.y, rc.x, rc.y, bz, wscale, sigma, s);
+                } else {
+                    coeff<NC>(rb.y, 0, 0, 0, wscale, sigma, s);
+                }
                 double wx[2], wy[2], wz[2];
-                weights1(r0.x, wx);
-                weights1(r0.y, wy);
-                weights1(r0.z, wz);
+                weights1(ra.x, wx);
+                weights1(ra.y, wy);
+                weights1(rb.x, wz);
 #pragma unroll
                 for (int c = 0; c < NC; ++c)
                     sh_s[lane * L::SS + c] = s[c];
@@ -230,6 +293,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     sh_w[a * L::WS + lane] = (wx[a >> 2] * wy[(a >> 1) & 1]) * wz[a & 1];
             }
             __syncwarp();
+            buf ^= 1u;
             const double *wrow = sh_w + (lane >> 2) * L::WS + (lane & 3);
             const double *srow = sh_s + (lane & 3) * L::SS;
             auto batch = [&](int kb) {
@@ -262,11 +326,9 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
             if (nbin < nbins) {
                 nb0 = seg_begin[nbin];
                 nb1 = seg_begin[nbin + 1];
-                if (lane < nb1 - nb0) {
-                    p0 = ld256(rec + 8 * (int64_t)(nb0 + lane));
-                    if (NC == 9)
-                        p1 = ld256(rec + 8 * (int64_t)(nb0 + lane) + 4);
-                }
+                if (lane == 0 && nb1 > nb0)
+                    tma_load(&s_rec[warp][buf][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
+                             &s_bar[warp][buf]);
             }
         } else {
             // ---- deposit: stage D[a][b][c], then RED in address order via the table
@@ -296,7 +358,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
         b0 = nb0;
         b1 = nb1;
         if (lane == 0 && bin < nbins)
-            tnext = atomicAdd(work, 1);
+            tnext = atom_add(work, 1);
     }
 }
 
@@ -319,9 +381,9 @@ struct O2 {
     static constexpr int CH = 32;                    // particles per chunk
     static constexpr int WS = 36;                    // weight tile row stride (doubles)
     static constexpr int WBUF = 32 * WS;             // one weight tile [32 nodes][WS]
-    static constexpr int STAGE = 729 * NC;
-    static constexpr int GROUP_DOUBLES = 2 * WBUF + STAGE + 32;  // + 27 row pointers
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 + 8 * GPC;
+    static constexpr int STAGE = 378 * NC;          // upper triangle (a <= b) of the 27x27 block
+    static constexpr int GROUP_DOUBLES = 2 * 256 + 2 * WBUF + STAGE + 32 + 2;  // recs, W, stage, rowp, mbar
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 * 2 + 8 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -365,29 +427,40 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     const int gtid = threadIdx.x - grp * L::WPG * 32;  // thread index inside the group
     constexpr int GT = L::WPG * 32;                     // threads per group
     double *gsm = dsm + grp * L::GROUP_DOUBLES;
-    double *wbuf = gsm;                        // [2][32 nodes][WS]
-    double *stage = gsm + 2 * L::WBUF;         // [27][27][NC]
+    double *srec = gsm;                        // [2][32 records][8]  (TMA-staged chunks)
+    double *wbuf = gsm + 2 * 256;              // [2][32 nodes][WS]
+    double *stage = wbuf + 2 * L::WBUF;        // [378 upper pairs][NC]
     double **rowp = reinterpret_cast<double **>(stage + L::STAGE);  // [27]
-    int16_t *s_slot = reinterpret_cast<int16_t *>(dsm + L::GPC * L::GROUP_DOUBLES);  // [27][27]
-    int64_t *s_bin = reinterpret_cast<int64_t *>(s_slot + 732) + grp;  // next-bin broadcast (8-B aligned)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 32);  // [2]
+    int16_t *s_slot = reinterpret_cast<int16_t *>(dsm + L::GPC * L::GROUP_DOUBLES);  // [27][27] slot(b-a)
+    int16_t *s_tri = s_slot + 730;                                                    // [27][27] upper index
+    int64_t *s_bin = reinterpret_cast<int64_t *>(s_tri + 730) + grp;  // next-bin broadcast (8-B aligned)
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * NC;
 
     for (int e = threadIdx.x; e < 729; e += blockDim.x) {
         const int a = e / 27, b = e - 27 * a;
         s_slot[e] = (int16_t)((b / 9 - a / 9 + 2) * 25 + ((b / 3) % 3 - (a / 3) % 3 + 2) * 5 + (b % 3 - a % 3 + 2));
+        const int i = a < b ? a : b, j = a < b ? b : a;
+        s_tri[e] = (int16_t)(i * 27 - i * (i - 1) / 2 + (j - i));
     }
     // dynamic, in-order bin scheduling; the next ticket is always one bin ahead
     int tnext = 0;
+    int64_t issued = -1;  // (gtid 0) bin whose first chunk is in flight
     if (gtid == 0) {
-        *s_bin = atomicAdd(work, 1);
-        tnext = atomicAdd(work, 1);
+        *s_bin = atom_add(work, 1);
+        tnext = atom_add(work, 1);
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
     }
     __syncthreads();
     int64_t bin = *s_bin;
-    int chunk = 0;  // global chunk counter -> weight buffer parity
+    int chunk = 0;  // global chunk counter -> buffer (chunk & 1), mbarrier parity (chunk >> 1) & 1
     while (bin < nbins) {
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
+        if (gtid == 0 && b1 > b0 && issued != bin)
+            tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(L::CH, b1 - b0) * 64, &bars[chunk & 1]);
         double acc[10][2];
 #pragma unroll
         for (int t = 0; t < 10; ++t)
@@ -395,14 +468,18 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         for (int base = b0; base < b1; base += L::CH, ++chunk) {
             const int m = min(L::CH, b1 - base);
             double *wt = wbuf + (chunk & 1) * L::WBUF;
-            // prep (every warp, lane = particle): s^comp and this warp's W rows
+            // prep (every warp, lane = particle): s^comp and this warp's W rows, from the
+            // TMA-staged record chunk
+            mbar_wait(&bars[chunk & 1], (chunk >> 1) & 1);
             double s_me = 0.0;
             if (lane < m) {
-                const double *r = rec + 8 * (int64_t)(base + lane);
-                const double4 r0 = ld256(r);
+                const double *r = srec + (chunk & 1) * 256 + 8 * lane;
+                const double2 ra = *reinterpret_cast<const double2 *>(r);
+                const double2 rb = *reinterpret_cast<const double2 *>(r + 2);
+                const double4 r0 = make_double4(ra.x, ra.y, rb.x, rb.y);
                 if (NC == 9) {
-                    const double4 r1 = ld256(r + 4);
-                    s_me = coeff_one(comp, r0.w, r1.x, r1.y, r1.z, wscale, sigma);
+                    const double2 rc = *reinterpret_cast<const double2 *>(r + 4);
+                    s_me = coeff_one(comp, r0.w, rc.x, rc.y, r[6], wscale, sigma);
                 } else {
                     s_me = sigma * r0.w;
                 }
@@ -416,6 +493,24 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                     wt[a * L::WS + lane] = a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
             }
             group_sync(GT, 1 + grp);
+            // every warp is past its reads of the other record buffer: prefetch the next chunk
+            if (gtid == 0) {
+                const double *src = nullptr;
+                int cnt = 0;
+                if (base + L::CH < b1) {
+                    src = rec + 8 * (int64_t)(base + L::CH);
+                    cnt = min(L::CH, b1 - base - L::CH);
+                } else if (tnext < nbins) {
+                    const int n0 = seg_begin[tnext], n1 = seg_begin[tnext + 1];
+                    if (n1 > n0) {
+                        src = rec + 8 * (int64_t)n0;
+                        cnt = min(L::CH, n1 - n0);
+                        issued = tnext;
+                    }
+                }
+                if (cnt)
+                    tma_load(srec + ((chunk + 1) & 1) * 256, src, cnt * 64, &bars[(chunk + 1) & 1]);
+            }
             const double *wcol = wt + (lane >> 2) * L::WS + (lane & 3);
             auto batch = [&](int kb) {
                 double w[4];
@@ -451,7 +546,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             if (gtid == 0) {
                 *s_bin = tnext;
                 if (tnext < nbins)
-                    tnext = atomicAdd(work, 1);
+                    tnext = atom_add(work, 1);
             }
             group_sync(GT, 1 + grp);
             bin = *s_bin;
@@ -469,7 +564,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         if (gtid == 0) {
             *s_bin = tnext;
             if (tnext < nbins)
-                tnext = atomicAdd(work, 1);
+                tnext = atom_add(work, 1);
         }
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
@@ -479,11 +574,8 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
                 const int b = 8 * tc + 2 * (lane & 3) + v;
-                if (a < 27 && b < 27) {
-                    stage[(a * 27 + b) * NC + comp] = acc[t][v];
-                    if (tr != tc)
-                        stage[(b * 27 + a) * NC + comp] = acc[t][v];
-                }
+                if (a < 27 && b < 27 && a <= b)  // M_ab = M_ba (eq_spatial_symmetry): keep a <= b
+                    stage[(a * 27 - a * (a - 1) / 2 + (b - a)) * NC + comp] = acc[t][v];
             }
         }
         group_sync(GT, 1 + grp);
@@ -496,14 +588,15 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                 const int a = run / 9, j = run - 9 * a;
                 const int ab0 = a * 27 + 9 * (j / 3) + 3 * (j % 3);
                 if (lane < 27) {
-                    const double v = stage[ab0 * 9 + lane];
+                    const int bz = lane / 9, c = lane - 9 * bz;
+                    const double v = stage[s_tri[ab0 + bz] * 9 + c];
                     if (v != 0.0)
                         red_add(rowp[a] + s_slot[ab0] * 9 + lane, v);
                 }
             }
         } else {
             for (int e = gtid; e < 729; e += GT) {
-                const double v = stage[e];
+                const double v = stage[s_tri[e]];
                 if (v != 0.0)
                     red_add(rowp[e / 27] + s_slot[e], v);
             }
@@ -524,6 +617,30 @@ unsigned grid_for(K kernel, int64_t items)
     int64_t want = (items + WARPS - 1) / WARPS;
     int64_t cap = (int64_t)sms * per_sm;
     return (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+template <int NC>
+cudaError_t launch_o1(const Geo &geo, const AsmArgs &a, cudaStream_t s)
+{
+    using L = O1<NC>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_asm_o1<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        if (e)
+            return e;
+        attr = true;
+    }
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o1<NC>, WARPS * 32, L::SMEM);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (a.nbins + WARPS - 1) / WARPS;
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+    k_asm_o1<NC><<<grid, WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
+                                                   a.ghost, a.work);
+    count_launch();
+    return cudaGetLastError();
 }
 
 template <int NC>
@@ -557,13 +674,9 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
     if (a.nbins == 0)
         return cudaSuccess;
     if (geo.order == 1) {
-        if (a.ncomp == 9) {
-            k_asm_o1<9><<<grid_for(k_asm_o1<9>, a.nbins), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost, a.work);
-        } else {
-            k_asm_o1<1><<<grid_for(k_asm_o1<1>, a.nbins), WARPS * 32, 0, s>>>(
-                geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out, a.ghost, a.work);
-        }
+        if (a.ncomp == 9)
+            return launch_o1<9>(geo, a, s);
+        return launch_o1<1>(geo, a, s);
     } else {
         if (a.ncomp == 9)
             return launch_o2<9>(geo, a, s);
