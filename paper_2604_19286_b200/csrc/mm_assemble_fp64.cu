@@ -122,13 +122,14 @@ __device__ __forceinline__ void weights2(double xi, double w[3])
     w[2] = 0.5 * (1.5 - t2) * (1.5 - t2);  // 1/2 <= |t2| <= 3/2
 }
 
-// Atomic ticket (inline PTX: keeps the compiler from warp-aggregating it, which would
-// broadcast the result with a shuffle right after the atomic and expose its latency).
-__device__ __forceinline__ int atom_add(int *p, int v)
+// Work ticket: atom.inc with limit 2^31-1 (== +1 for any reachable count).  Unlike atom.add,
+// ptxas does not warp-aggregate inc (it is not associative), so no shuffle of the result
+// is placed right after the atomic and the ticket can be requested one bin ahead.
+__device__ __forceinline__ int atom_add(int *p, int /*one*/)
 {
-    int r;
-    asm volatile("atom.global.add.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(v) : "memory");
-    return r;
+    unsigned r;
+    asm volatile("atom.global.inc.u32 %0, [%1], %2;" : "=r"(r) : "l"(p), "r"(0x7fffffffu) : "memory");
+    return (int)r;
 }
 
 // ---- mbarrier + TMA bulk copy (cp.async.bulk) helpers -------------------------------
