@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
     double *sh_s = sm + 8 * L::WS;
     const int plane = g.n1 * g.n2;
     constexpr int RL = 27 * NC;
+    (void)work;
 
     // deposit table (per CTA): element e of D[a][b][c] in address order ->
     // node a (3 bits) | offset (slot*NC + c) within node a's row
@@ -224,52 +225,48 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
     }
     __syncthreads();
 
-    // Software pipeline: the next bin's ticket and the next chunk's records (one 2-KB
-    // cp.async.bulk per chunk into a double-buffered shared-memory slot) are requested one
-    // chunk ahead, so neither latency is exposed at a bin/chunk boundary.
-    int t0 = 0, tnext = 0;
-    if (lane == 0) {
-        t0 = atom_add(work, 1);  // dynamic, in-order bin scheduling (L2 locality, balance)
-        tnext = atom_add(work, 1);
-    }
-    int64_t bin = __shfl_sync(0xffffffffu, t0, 0);
-    int b0 = 0, b1 = 0;
-    uint32_t buf = 0, phases = 0u;  // bit b: expected parity of buffer b's mbarrier
+    // Static interleaved schedule (warp w: bins w, w + W, ...): consecutive warps work on
+    // consecutive bins (L2 locality of the deposits) and every future bin is known, so the
+    // bin ranges are loaded one bin ahead and each 2-KB record chunk is fetched with one
+    // cp.async.bulk into a double-buffered shared-memory slot one chunk ahead.
+    const int nw = gridDim.x * WARPS;
+    int bin = blockIdx.x * WARPS + warp;
+    int b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
     if (bin < nbins) {
-        b0 = seg_begin[bin];
-        b1 = seg_begin[bin + 1];
-        if (lane == 0 && b1 > b0)
-            tma_load(&s_rec[warp][0][0], rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &s_bar[warp][0]);
+        b0 = __ldg(seg_begin + bin);
+        b1 = __ldg(seg_begin + bin + 1);
     }
+    if (bin + nw < nbins) {
+        nb0 = __ldg(seg_begin + bin + nw);
+        nb1 = __ldg(seg_begin + bin + nw + 1);
+    }
+    uint32_t chunk = 0;  // buffer (chunk & 1), mbarrier parity (chunk >> 1) & 1
+    if (lane == 0 && bin < nbins && b1 > b0)
+        tma_load(&s_rec[warp][0][0], rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &s_bar[warp][0]);
     while (bin < nbins) {
+        // bin ranges two bins ahead (consumed when this bin's successor prefetches)
+        int nn0 = 0, nn1 = 0;
+        if (bin + 2 * nw < nbins) {
+            nn0 = __ldg(seg_begin + bin + 2 * nw);
+            nn1 = __ldg(seg_begin + bin + 2 * nw + 1);
+        }
         double acc[NC][2];
 #pragma unroll
         for (int c = 0; c < NC; ++c)
             acc[c][0] = acc[c][1] = 0.0;
-        int64_t nbin = nbins;
-        int nb0 = 0, nb1 = 0;
-        for (int base = b0; base < b1; base += 32) {
+        for (int base = b0; base < b1; base += 32, ++chunk) {
             const int m = min(32, b1 - base);
+            const uint32_t buf = chunk & 1u;
             // prefetch the next chunk of this bin, else the first chunk of the next bin
-            int pf = -1, pfn = 0;
-            if (base + 32 < b1) {
-                pf = base + 32;
-                pfn = min(32, b1 - pf);
-            } else {
-                nbin = __shfl_sync(0xffffffffu, tnext, 0);
-                if (nbin < nbins) {
-                    nb0 = seg_begin[nbin];
-                    nb1 = seg_begin[nbin + 1];
-                    if (nb1 > nb0) {
-                        pf = nb0;
-                        pfn = min(32, nb1 - nb0);
-                    }
-                }
+            if (lane == 0) {
+                if (base + 32 < b1)
+                    tma_load(&s_rec[warp][buf ^ 1][0], rec + 8 * (int64_t)(base + 32), min(32, b1 - base - 32) * 64,
+                             &s_bar[warp][buf ^ 1]);
+                else if (bin + nw < nbins && nb1 > nb0)
+                    tma_load(&s_rec[warp][buf ^ 1][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
+                             &s_bar[warp][buf ^ 1]);
             }
-            if (lane == 0 && pf >= 0)
-                tma_load(&s_rec[warp][buf ^ 1][0], rec + 8 * (int64_t)pf, pfn * 64, &s_bar[warp][buf ^ 1]);
-            mbar_wait(&s_bar[warp][buf], (phases >> buf) & 1u);
-            phases ^= 1u << buf;
+            mbar_wait(&s_bar[warp][buf], (chunk >> 1) & 1u);
             if (lane < m) {
                 const double *r = &s_rec[warp][buf][8 * lane];
                 const double2 ra = *reinterpret_cast<const double2 *>(r);      // xi_x, xi_y
@@ -277,8 +274,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                 double s[NC];
                 if (NC == 9) {
                     const double2 rc = *reinterpret_cast<const double2 *>(r + 4);  // Bx, By
-                    const double bz = r[6];
-                    coeff<NC>(rb.y, rc.x, rc.y, bz, wscale, sigma, s);
+                    coeff<NC>(rb.y, rc.x, rc.y, r[6], wscale, sigma, s);
                 } else {
                     coeff<NC>(rb.y, 0, 0, 0, wscale, sigma, s);
                 }
@@ -294,7 +290,6 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     sh_w[a * L::WS + lane] = (wx[a >> 2] * wy[(a >> 1) & 1]) * wz[a & 1];
             }
             __syncwarp();
-            buf ^= 1u;
             const double *wrow = sh_w + (lane >> 2) * L::WS + (lane & 3);
             const double *srow = sh_s + (lane & 3) * L::SS;
             auto batch = [&](int kb) {
@@ -322,16 +317,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
             }
             __syncwarp();
         }
-        if (b0 == b1) {  // empty bin: nothing to deposit; fetch the following one
-            nbin = __shfl_sync(0xffffffffu, tnext, 0);
-            if (nbin < nbins) {
-                nb0 = seg_begin[nbin];
-                nb1 = seg_begin[nbin + 1];
-                if (lane == 0 && nb1 > nb0)
-                    tma_load(&s_rec[warp][buf][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
-                             &s_bar[warp][buf]);
-            }
-        } else {
+        if (b1 > b0) {
             // ---- deposit: stage D[a][b][c], then RED in address order via the table
 #pragma unroll
             for (int c = 0; c < NC; ++c) {
@@ -339,7 +325,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                 sm[(lane >> 2) * 8 * NC + (2 * (lane & 3) + 1) * NC + c] = acc[c][1];
             }
             // row pointers of the 8 support nodes: lane a (mod 8) computes node a's
-            const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+            const int bx = bin / plane, rem = bin - bx * plane;
             const int by = rem / g.n2, bz = rem - by * g.n2;
             const int a8 = lane & 7;
             double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
@@ -354,12 +340,16 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     red_add(row + (t >> 3), v);
             }
             __syncwarp();
+        } else if (lane == 0 && bin + nw < nbins && nb1 > nb0) {
+            // empty bin: nothing was prefetched for the successor yet
+            tma_load(&s_rec[warp][chunk & 1u][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
+                     &s_bar[warp][chunk & 1u]);
         }
-        bin = nbin;
+        bin += nw;
         b0 = nb0;
         b1 = nb1;
-        if (lane == 0 && bin < nbins)
-            tnext = atom_add(work, 1);
+        nb0 = nn0;
+        nb1 = nn1;
     }
 }
 
@@ -384,7 +374,7 @@ struct O2 {
     static constexpr int WBUF = 32 * WS;             // one weight tile [32 nodes][WS]
     static constexpr int STAGE = 378 * NC;          // upper triangle (a <= b) of the 27x27 block
     static constexpr int GROUP_DOUBLES = 2 * 256 + 2 * WBUF + STAGE + 32 + 2;  // recs, W, stage, rowp, mbar
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 * 2 + 8 * GPC;
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 * 2 + 8 * GPC + 32 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -445,12 +435,18 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         const int i = a < b ? a : b, j = a < b ? b : a;
         s_tri[e] = (int16_t)(i * 27 - i * (i - 1) / 2 + (j - i));
     }
-    // dynamic, in-order bin scheduling; the next ticket is always one bin ahead
-    int tnext = 0;
-    int64_t issued = -1;  // (gtid 0) bin whose first chunk is in flight
+    // dynamic, in-order bin scheduling.  Thread 0 of the group keeps a two-deep ticket
+    // queue (tnext = the bin after the current one, tnext2 = the one after that) so that
+    // the atomic, the bin-range loads and the first-chunk TMA of a bin are all issued at
+    // least one bin before they are needed.
+    // (thread 0 only; kept in shared memory to spare registers of the other 287 threads)
+    int *q = reinterpret_cast<int *>(s_bin + L::GPC) + 8 * grp;  // tnext, tnext2, -, -, issued
+    int tn0 = 0, tn1 = 0;                                         // (gtid 0) range of bin tnext
     if (gtid == 0) {
         *s_bin = atom_add(work, 1);
-        tnext = atom_add(work, 1);
+        q[0] = atom_add(work, 1);
+        q[1] = atom_add(work, 1);
+        q[4] = -1;
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
@@ -460,8 +456,16 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     int chunk = 0;  // global chunk counter -> buffer (chunk & 1), mbarrier parity (chunk >> 1) & 1
     while (bin < nbins) {
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
-        if (gtid == 0 && b1 > b0 && issued != bin)
-            tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(L::CH, b1 - b0) * 64, &bars[chunk & 1]);
+        if (gtid == 0) {
+            if (b1 > b0 && q[4] != bin)
+                tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(L::CH, b1 - b0) * 64, &bars[chunk & 1]);
+            const int tnext = q[0];
+            tn0 = tn1 = 0;
+            if (tnext < nbins) {  // loads in flight until the last chunk of this bin
+                tn0 = seg_begin[tnext];
+                tn1 = seg_begin[tnext + 1];
+            }
+        }
         double acc[10][2];
 #pragma unroll
         for (int t = 0; t < 10; ++t)
@@ -501,13 +505,10 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                 if (base + L::CH < b1) {
                     src = rec + 8 * (int64_t)(base + L::CH);
                     cnt = min(L::CH, b1 - base - L::CH);
-                } else if (tnext < nbins) {
-                    const int n0 = seg_begin[tnext], n1 = seg_begin[tnext + 1];
-                    if (n1 > n0) {
-                        src = rec + 8 * (int64_t)n0;
-                        cnt = min(L::CH, n1 - n0);
-                        issued = tnext;
-                    }
+                } else if (q[0] < nbins && tn1 > tn0) {
+                    src = rec + 8 * (int64_t)tn0;
+                    cnt = min(L::CH, tn1 - tn0);
+                    q[4] = q[0];
                 }
                 if (cnt)
                     tma_load(srec + ((chunk + 1) & 1) * 256, src, cnt * 64, &bars[(chunk + 1) & 1]);
@@ -545,9 +546,10 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         }
         if (b0 == b1) {  // empty bin (rare): just advance the ticket
             if (gtid == 0) {
-                *s_bin = tnext;
-                if (tnext < nbins)
-                    tnext = atom_add(work, 1);
+                *s_bin = q[0];
+                q[0] = q[1];
+                if (q[1] < nbins)
+                    q[1] = atom_add(work, 1);
             }
             group_sync(GT, 1 + grp);
             bin = *s_bin;
@@ -563,9 +565,10 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                               wrapi(bz + a % 3, g.n2), out, ghost, RL);
         }
         if (gtid == 0) {
-            *s_bin = tnext;
-            if (tnext < nbins)
-                tnext = atom_add(work, 1);
+            *s_bin = q[0];
+            q[0] = q[1];
+            if (q[1] < nbins)
+                q[1] = atom_add(work, 1);
         }
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
