@@ -374,7 +374,7 @@ struct O2 {
     static constexpr int WBUF = 32 * WS;             // one weight tile [32 nodes][WS]
     static constexpr int STAGE = 378 * NC;          // upper triangle (a <= b) of the 27x27 block
     static constexpr int GROUP_DOUBLES = 2 * 256 + 2 * WBUF + STAGE + 32 + 2;  // recs, W, stage, rowp, mbar
-    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + 730 * 2 * 2 + 8 * GPC + 32 * GPC;
+    static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + (730 * 2 + 640) * 2 + 8 * GPC + 32 * GPC;
 };
 
 __device__ __forceinline__ void group_sync(int nthreads, int id)
@@ -425,7 +425,8 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 32);  // [2]
     int16_t *s_slot = reinterpret_cast<int16_t *>(dsm + L::GPC * L::GROUP_DOUBLES);  // [27][27] slot(b-a)
     int16_t *s_tri = s_slot + 730;                                                    // [27][27] upper index
-    int64_t *s_bin = reinterpret_cast<int64_t *>(s_tri + 730) + grp;  // next-bin broadcast (8-B aligned)
+    int16_t *s_stoff = s_tri + 730;  // [10 tiles][2][32 lanes] stage offset of the lane's entry, -1 = none
+    int64_t *s_bin = reinterpret_cast<int64_t *>(s_stoff + 640) + grp;  // next-bin broadcast (8-B aligned)
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * NC;
 
@@ -434,6 +435,13 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         s_slot[e] = (int16_t)((b / 9 - a / 9 + 2) * 25 + ((b / 3) % 3 - (a / 3) % 3 + 2) * 5 + (b % 3 - a % 3 + 2));
         const int i = a < b ? a : b, j = a < b ? b : a;
         s_tri[e] = (int16_t)(i * 27 - i * (i - 1) / 2 + (j - i));
+    }
+    for (int e = threadIdx.x; e < 640; e += blockDim.x) {
+        const int t = e / 64, v = (e / 32) & 1, l = e & 31;
+        const int tr = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
+        const int tc = t < 4 ? t : (t < 7 ? t - 3 : (t < 9 ? t - 5 : 3));
+        const int a = 8 * tr + (l >> 2), b = 8 * tc + 2 * (l & 3) + v;
+        s_stoff[e] = (a < 27 && b < 27 && a <= b) ? (int16_t)(a * 27 - a * (a - 1) / 2 + (b - a)) : (int16_t)-1;
     }
     // dynamic, in-order bin scheduling.  Thread 0 of the group keeps a two-deep ticket
     // queue (tnext = the bin after the current one, tnext2 = the one after that) so that
@@ -494,8 +502,20 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                 weights2(r0.z, wz);
                 // runtime node digits: select instead of indexing (keeps wx/wy/wz in registers)
                 auto sel = [](const double *w, int i) { return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]); };
-                for (int a = comp; a < 32; a += L::WPG)
-                    wt[a * L::WS + lane] = a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
+                if (NC == 9) {
+                    // warp c owns nodes a = c + 9k: digits (k, c/3, c%3)
+                    const double wyc = sel(wy, comp / 3), wzc = sel(wz, comp % 3);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int a = comp + 9 * k;
+                        if (a < 32)
+                            wt[a * L::WS + lane] = a < 27 ? (wx[k < 3 ? k : 0] * wyc) * wzc : 0.0;
+                    }
+                } else {
+                    for (int a = 0; a < 32; ++a)
+                        wt[a * L::WS + lane] =
+                            a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
+                }
             }
             group_sync(GT, 1 + grp);
             // every warp is past its reads of the other record buffer: prefetch the next chunk
@@ -570,16 +590,14 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             if (q[1] < nbins)
                 q[1] = atom_add(work, 1);
         }
+        // M_ab = M_ba (eq_spatial_symmetry): keep the a <= b entries (table s_stoff)
 #pragma unroll
         for (int t = 0; t < 10; ++t) {
-            const int tr = t < 4 ? 0 : (t < 7 ? 1 : (t < 9 ? 2 : 3));
-            const int tc = t < 4 ? t : (t < 7 ? t - 3 : (t < 9 ? t - 5 : 3));
-            const int a = 8 * tr + (lane >> 2);
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-                const int b = 8 * tc + 2 * (lane & 3) + v;
-                if (a < 27 && b < 27 && a <= b)  // M_ab = M_ba (eq_spatial_symmetry): keep a <= b
-                    stage[(a * 27 - a * (a - 1) / 2 + (b - a)) * NC + comp] = acc[t][v];
+                const int o = s_stoff[(2 * t + v) * 32 + lane];
+                if (o >= 0)
+                    stage[o * NC + comp] = acc[t][v];
             }
         }
         group_sync(GT, 1 + grp);
@@ -588,12 +606,14 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         //      doubles (b_z = 0..2 x 9 comps) -> row(a) + slot(b0 - a)*9 + lane.  The next
         //      write of stage/rowp/s_bin comes after the next chunk barrier.
         if (NC == 9) {
-            for (int run = comp; run < 243; run += L::WPG) {
-                const int a = run / 9, j = run - 9 * a;
-                const int ab0 = a * 27 + 9 * (j / 3) + 3 * (j % 3);
-                if (lane < 27) {
-                    const int bz = lane / 9, c = lane - 9 * bz;
-                    const double v = stage[s_tri[ab0 + bz] * 9 + c];
+            // warp c flushes runs (a, b_x, b_y) = (a, c/3, c%3) for a = 0..26
+            const int b0c = 9 * (comp / 3) + 3 * (comp % 3);
+            const int bzl = lane / 9, cl = lane - 9 * bzl;
+            if (lane < 27) {
+#pragma unroll 3
+                for (int a = 0; a < 27; ++a) {
+                    const int ab0 = a * 27 + b0c;
+                    const double v = stage[s_tri[ab0 + bzl] * 9 + cl];
                     if (v != 0.0)
                         red_add(rowp[a] + s_slot[ab0] * 9 + lane, v);
                 }
