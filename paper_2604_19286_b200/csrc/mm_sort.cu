@@ -16,6 +16,7 @@
 //              write pad slots; warp path (<= 1024), CTA path (<= 16384), huge path
 //   k_scatter  coalesced over particles: rec[dest[p]] = {xi, q, B, 0} (64-B records)
 #include <climits>
+#include <cstdlib>
 
 #include "mm_internal.cuh"
 
@@ -283,6 +284,31 @@ __device__ __forceinline__ void st256(double *p, double a, double b, double c, d
 }
 
 
+// Record of particle p written to sorted slot i (gather mode: coalesced writes, random reads).
+struct Gather {
+    Geo g;
+    const double *pos, *q, *B;
+    double *rec;
+    int32_t *status;
+    int on;
+};
+
+__device__ __forceinline__ void gather_record(const Gather &G, int64_t i, int64_t p)
+{
+    Located L = locate(G.g, __ldg(G.pos + 3 * p), __ldg(G.pos + 3 * p + 1), __ldg(G.pos + 3 * p + 2));
+    const double qq = __ldg(G.q + p);
+    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
+    if (G.B) {
+        b0 = __ldg(G.B + 3 * p);
+        b1 = __ldg(G.B + 3 * p + 1);
+        b2 = __ldg(G.B + 3 * p + 2);
+    }
+    if (!(isfinite(qq) && isfinite(b0) && isfinite(b1) && isfinite(b2)))
+        atomicOr(&G.status[ST_ERR], ERR_NONFINITE);
+    st256(G.rec + 8 * i, L.xi[0], L.xi[1], L.xi[2], qq);
+    st256(G.rec + 8 * i + 4, b0, b1, b2, 0.0);
+}
+
 __device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int64_t from, int64_t to, int tid,
                                           int nthr)
 {
@@ -298,7 +324,7 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
                                                              int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                              double *__restrict__ rec, int32_t *__restrict__ mid_list,
                                                              int32_t *__restrict__ huge_list,
-                                                             int32_t *__restrict__ status)
+                                                             int32_t *__restrict__ status, Gather G)
 {
     __shared__ int32_t buf[FIX_WARPS][WARP_BIN_MAX];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -342,11 +368,17 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
             }
             if (lane < n) {
                 perm[b + lane] = v0;
-                dest[v0] = (int32_t)(b + lane);
+                if (G.on)
+                    gather_record(G, b + lane, v0);
+                else
+                    dest[v0] = (int32_t)(b + lane);
             }
             if (lane + 32 < n) {
                 perm[b + lane + 32] = v1;
-                dest[v1] = (int32_t)(b + lane + 32);
+                if (G.on)
+                    gather_record(G, b + lane + 32, v1);
+                else
+                    dest[v1] = (int32_t)(b + lane + 32);
             }
             continue;
         }
@@ -375,7 +407,10 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
         for (int i = lane; i < n; i += 32) {
             int32_t v = s[i];
             perm[b + i] = v;
-            dest[v] = (int32_t)(b + i);
+            if (G.on)
+                gather_record(G, b + i, v);
+            else
+                dest[v] = (int32_t)(b + i);
         }
         __syncwarp();
     }
@@ -385,7 +420,7 @@ __global__ void __launch_bounds__(1024) k_fix_cta(const int32_t *__restrict__ co
                                                   const int32_t *__restrict__ seg_begin,
                                                   int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                   const int32_t *__restrict__ mid_list,
-                                                  const int32_t *__restrict__ status)
+                                                  const int32_t *__restrict__ status, Gather G)
 {
     extern __shared__ int32_t s[];
     const int nmid = status[ST_NMID];
@@ -418,7 +453,10 @@ __global__ void __launch_bounds__(1024) k_fix_cta(const int32_t *__restrict__ co
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             int32_t v = s[i];
             perm[b + i] = v;
-            dest[v] = (int32_t)(b + i);
+            if (G.on)
+                gather_record(G, b + i, v);
+            else
+                dest[v] = (int32_t)(b + i);
         }
         __syncthreads();
     }
@@ -430,7 +468,7 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
                                                    const int32_t *__restrict__ seg_begin,
                                                    int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                    const int32_t *__restrict__ huge_list,
-                                                   const int32_t *__restrict__ status)
+                                                   const int32_t *__restrict__ status, Gather G)
 {
     const int nhuge = status[ST_NHUGE];
     for (int it = blockIdx.x; it < nhuge; it += gridDim.x) {
@@ -443,7 +481,10 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
             int pre = block_excl_scan(f, total);
             if (f) {
                 perm[out + pre] = (int32_t)p;
-                dest[p] = (int32_t)(out + pre);
+                if (G.on)
+                    gather_record(G, out + pre, p);
+                else
+                    dest[p] = (int32_t)(out + pre);
             }
             out += total;
         }
@@ -528,6 +569,13 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         return e;
     const int T = 256;
     const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
+    // record pass: scatter (coalesced reads, random 64-B writes) or gather in the per-bin
+    // fix-up (random reads, coalesced writes); MM_SORT_GATHER=1 selects the latter
+    static const int gather_env = [] {
+        const char *v = getenv("MM_SORT_GATHER");
+        return v && v[0] == '1' ? 1 : 0;
+    }();
+    Gather G{geo, b.pos, b.q, b.B, b.rec, b.status, gather_env};
     if (b.np > 0) {
         if (vec)
             k_key<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
@@ -550,7 +598,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         if (grid < 1)
             grid = 1;
         k_fix_warp<<<grid, FIX_WARPS * 32, 0, s>>>(b.nbins, b.count, b.seg_begin, b.perm, b.rank, b.rec,
-                                                   b.mid_list, b.huge_list, b.status);
+                                                   b.mid_list, b.huge_list, b.status, G);
         count_launch();
     }
     if (b.np > WARP_BIN_MAX) {
@@ -561,14 +609,14 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
                 return e;
             attr = true;
         }
-        k_fix_cta<<<148, 1024, CTA_BIN_MAX * 4, s>>>(b.count, b.seg_begin, b.perm, b.rank, b.mid_list, b.status);
+        k_fix_cta<<<148, 1024, CTA_BIN_MAX * 4, s>>>(b.count, b.seg_begin, b.perm, b.rank, b.mid_list, b.status, G);
         count_launch();
     }
     if (b.np > CTA_BIN_MAX) {
-        k_fix_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.seg_begin, b.perm, b.rank, b.huge_list, b.status);
+        k_fix_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.seg_begin, b.perm, b.rank, b.huge_list, b.status, G);
         count_launch();
     }
-    if (b.np > 0) {
+    if (b.np > 0 && !G.on) {
         if (vec)
             k_scatter<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
                                                                       b.rec, b.status);
