@@ -309,6 +309,34 @@ __device__ __forceinline__ void gather_record(const Gather &G, int64_t i, int64_
     st256(G.rec + 8 * i + 4, b0, b1, b2, 0.0);
 }
 
+// Register bitonic network over K = 32 or 64 keys (2 per lane), fully unrolled so the
+// partner distances and directions are compile-time constants.
+template <int K>
+__device__ __forceinline__ void bitonic_reg(int32_t &v0, int32_t &v1, int lane)
+{
+#pragma unroll
+    for (int k = 2; k <= K; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j == 32) {
+                const int32_t lo = min(v0, v1), hi = max(v0, v1);
+                v0 = lo;  // k == 64: every index ascends
+                v1 = hi;
+            } else {
+                const bool lower = (lane & j) == 0;
+                const int32_t p0 = __shfl_xor_sync(0xffffffffu, v0, j);
+                const bool up0 = (lane & k) == 0;
+                v0 = (lower == up0) ? min(v0, p0) : max(v0, p0);
+                if (K == 64) {
+                    const int32_t p1 = __shfl_xor_sync(0xffffffffu, v1, j);
+                    const bool up1 = ((lane + 32) & k) == 0;
+                    v1 = (lower == up1) ? min(v1, p1) : max(v1, p1);
+                }
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int64_t from, int64_t to, int tid,
                                           int nthr)
 {
@@ -346,26 +374,13 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
             continue;
         }
         if (n <= 64) {
-            // bitonic sort of 64 keys held as (v0 = elem lane, v1 = elem lane + 32), via shuffles
+            // bitonic sort of the bin's keys held as (v0 = elem lane, v1 = elem lane + 32)
             int32_t v0 = lane < n ? perm[b + lane] : INT_MAX;
             int32_t v1 = lane + 32 < n ? perm[b + lane + 32] : INT_MAX;
-            const int K = n <= 32 ? 32 : 64;
-            for (int k = 2; k <= K; k <<= 1) {
-                for (int j = k >> 1; j > 0; j >>= 1) {
-                    if (j == 32) {
-                        int32_t lo = min(v0, v1), hi = max(v0, v1);
-                        v0 = lo;
-                        v1 = hi;  // k == 64: index lane has (lane & 64) == 0 -> ascending
-                    } else {
-                        const bool lower = (lane & j) == 0;
-                        int32_t p0 = __shfl_xor_sync(0xffffffffu, v0, j);
-                        int32_t p1 = __shfl_xor_sync(0xffffffffu, v1, j);
-                        const bool up0 = (lane & k) == 0, up1 = ((lane + 32) & k) == 0;
-                        v0 = (lower == up0) ? min(v0, p0) : max(v0, p0);
-                        v1 = (lower == up1) ? min(v1, p1) : max(v1, p1);
-                    }
-                }
-            }
+            if (n <= 32)
+                bitonic_reg<32>(v0, v1, lane);
+            else
+                bitonic_reg<64>(v0, v1, lane);
             if (lane < n) {
                 perm[b + lane] = v0;
                 if (G.on)
