@@ -111,23 +111,34 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def oracle_rate(cfg, d, budget_s=12.0):
-    """Oracle (plain single-thread FP64 C loop) on a bounded sample of the workload."""
+def _oracle_cost(cfg, d):
+    """(fixed seconds per call, seconds per particle) of the oracle on this workload: two short
+    calls of 20k and 100k particles (the fixed part is the whole-grid output zeroing)."""
     import oracle
-    n = cfg.n
     kind = cfg.ncomp
-    m = min(len(d["q"]), 20000)
+    ts = []
+    for m in (20000, 100000):
+        m = min(m, len(d["q"]))
+        t0 = time.perf_counter()
+        oracle.assemble(cfg.n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
+        ts.append((m, time.perf_counter() - t0))
+    (m1, t1), (m2, t2) = ts
+    b = max((t2 - t1) / max(m2 - m1, 1), 1e-9)
+    return max(t1 - b * m1, 0.0), b
+
+
+def oracle_rate(cfg, d, budget_s=12.0):
+    """Oracle (plain single-thread FP64 C loop) on a bounded sample (~budget_s) of the workload."""
+    import oracle
+    a, b = _oracle_cost(cfg, d)
+    kind = cfg.ncomp
+    m = int(min(len(d["q"]), max(20000, (budget_s - a) / b)))
     t0 = time.perf_counter()
-    oracle.assemble(n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
-    t1 = time.perf_counter() - t0
-    # scale the sample to ~budget_s of CPU work (the output array memset is part of the oracle)
-    m2 = int(min(len(d["q"]), max(m, m * budget_s / max(t1, 1e-3))))
-    t0 = time.perf_counter()
-    oracle.assemble(n, cfg.order, kind, d["pos"][:m2], d["q"][:m2], d["B"][:m2] if kind == 9 else None)
-    t2 = time.perf_counter() - t0
-    return {"value": m2 / t2 / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"first {m2} of {len(d['q'])} particles of {cfg.name} (input order), whole {n} grid output,"
-                      f" {t2:.1f} s single-threaded on {os.cpu_count()} host cores"}
+    oracle.assemble(cfg.n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
+    t = time.perf_counter() - t0
+    return {"value": m / t / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"first {m} of {len(d['q'])} particles of {cfg.name} (input order) into the whole "
+                      f"{'x'.join(map(str, cfg.n))} grid, {t:.1f} s single-threaded (host has {os.cpu_count()} cores)"}
 
 
 def run_reference(args):
@@ -137,8 +148,11 @@ def run_reference(args):
     cfg = synth.config("c2")
     d = synth.particles(cfg)
     import oracle
+    # bounded sample per step so that the whole --steps/--warmup run takes ~150 s of host time
+    a, b = _oracle_cost(cfg, d)
+    per_step = 150.0 / max(args.steps + args.warmup, 1)
+    m = int(min(len(d["q"]) // 2, max(2000, (per_step - a) / b)))
     steps = []
-    m = 200000 // 4
     for _ in range(args.warmup):
         oracle.assemble(cfg.n, 1, 9, d["pos"][:m], d["q"][:m], d["B"][:m])
     for k in range(args.steps):

@@ -44,9 +44,10 @@ def raw(rep):
     hdr, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        d = {"Kernel Name": r[hdr.index("Kernel Name")]}
+        d = {}
         for i, h in enumerate(hdr):
             d[h] = (r[i], units[i])
+        d["Kernel Name"] = r[hdr.index("Kernel Name")]
         res.append((d, hdr, r))
     return res
 
@@ -96,9 +97,10 @@ def main():
                 v, u = d[key]
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
-            if "k_asm_o1<9>" in name and "dram__bytes_read.sum" in d:
+            nm = name.replace("(int)", "").replace(" ", "")
+            if "k_asm_o1<9>" in nm and "dram__bytes_read.sum" in d:
                 traffic["assemble_o1_bytes_per_launch"] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
-            if "k_asm_o2<9>" in name and "dram__bytes_read.sum" in d:
+            if "k_asm_o2<9>" in nm and "dram__bytes_read.sum" in d:
                 traffic["assemble_o2_bytes_per_launch"] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
     lc = os.path.join(a.src, "launches.csv")
     if os.path.exists(lc):
