@@ -61,9 +61,10 @@ typedef enum {
 typedef enum { MM_SCALAR = 1, MM_TENSOR = 9 } mm_kind; /* value = components C */
 
 typedef enum {
-    MM_FP64 = 0,   /* FP64 operands, FP64 DMMA 8x8x4 tiles, FP64 output       */
-    MM_TF32 = 1,   /* reserved: TF32 operands, FP32 accumulation/output       */
-    MM_TF32X3 = 2  /* reserved: split-TF32 (3 products), FP32 output           */
+    MM_FP64 = 0,   /* FP64 operands, FP64 DMMA 8x8x4 tiles (mma.sync), FP64 output        */
+    MM_TF32 = 1,   /* TF32 operands (cvt.rna), FP32 accumulation in TMEM (tcgen05.mma
+                      kind::tf32), FP32 output                                         */
+    MM_TF32X3 = 2  /* split TF32 x = hi + lo, D += AhBh + AhBl + AlBh, FP32 output      */
 } mm_precision;
 
 typedef struct {
@@ -148,13 +149,14 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  *
  *   h          sorted handle (mm_sort_by_cell) for the same grid
  *   kind       MM_SCALAR | MM_TENSOR (MM_TENSOR needs a handle sorted with B)
- *   prec       MM_FP64 (MM_TF32/MM_TF32X3 return MM_ERR_INCOMPATIBLE in this
- *              version)
+ *   prec       MM_FP64 (DMMA, FP64 out) | MM_TF32 | MM_TF32X3 (tcgen05 kind::tf32,
+ *              FP32 out; the TF32 variant "reported separately")
  *   sp         host, species constants (qom, dt, c > 0, sigma)
  *   accumulate 0: out = M (the owned rows are overwritten);
  *              1: out += M (species sum)
- *   out        device, FP64 [(x_end-x_begin)*n1*n2][S][C] (layout above)
- *   ghost      device, FP64 [mm_ghost_planes(order)][n1*n2][S][C], required
+ *   out        device, [(x_end-x_begin)*n1*n2][S][C] (layout above); FP64 for
+ *              MM_FP64, FP32 for MM_TF32 / MM_TF32X3
+ *   ghost      device, same element type, [mm_ghost_planes(order)][n1*n2][S][C], required
  *              when the grid is a slab (x_begin > 0 or x_end < n[0]) and
  *              ignored (may be NULL) otherwise.  Rows of nodes outside the
  *              slab are added here: order 1 -> plane 0 = node plane x_end;
@@ -165,10 +167,10 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  * stream has passed this call.
  */
 mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp,
-                      int accumulate, double *out, double *ghost, void *stream);
+                      int accumulate, void *out, void *ghost, void *stream);
 
 /*
- * mm_ghost_add — add `nplanes` received ghost node planes into owned rows
+ * mm_ghost_add — add `nplanes` received ghost node planes into owned rows (FP64 output)
  * (the reduction step of the slab decomposition):
  *   out[((first_plane + k)*n1*n2 + r)*S*C + e] += recv[(k*n1*n2 + r)*S*C + e]
  * for k < nplanes.  `first_plane` is relative to x_begin.  Asynchronous.

@@ -207,10 +207,13 @@ def is_slab(grid: mm_grid) -> bool:
 
 def mm_assemble(handle: Sorted, kind: int, prec: int, species: mm_species, out, ghost=None,
                 accumulate: bool = False, stream=None):
-    """Assemble the mass matrix of one species into `out` (and `ghost` for slabs)."""
+    """Assemble the mass matrix of one species into `out` (and `ghost` for slabs).
+
+    `out`/`ghost` are float64 for MM_FP64 and float32 for MM_TF32 / MM_TF32X3."""
     lib = load_library()
+    dt = torch.float64 if int(prec) == MM_FP64 else torch.float32
     st = lib.mm_assemble(handle.ptr, int(kind), int(prec), ctypes.byref(species), int(bool(accumulate)),
-                         _dev_ptr(out, name="out"), _dev_ptr(ghost, name="ghost") if ghost is not None else None,
+                         _dev_ptr(out, dt, name="out"), _dev_ptr(ghost, dt, name="ghost") if ghost is not None else None,
                          _stream_ptr(stream))
     _check(st)
     return out

@@ -306,7 +306,7 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)
 }
 
 mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, int accumulate,
-                      double *out, double *ghost, void *stream)
+                      void *out, void *ghost, void *stream)
 {
     try {
         if (!h || !sp || !out)
@@ -315,8 +315,8 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
             return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
         if (kind != MM_SCALAR && kind != MM_TENSOR)
             return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
-        if (prec != MM_FP64)
-            return fail(MM_ERR_INCOMPATIBLE, "precision %d not available in this build (MM_FP64 only)", (int)prec);
+        if (prec != MM_FP64 && prec != MM_TF32 && prec != MM_TF32X3)
+            return fail(MM_ERR_INVALID_ARG, "precision must be MM_FP64, MM_TF32 or MM_TF32X3");
         if (kind == MM_TENSOR && !h->has_B && h->np > 0)
             return fail(MM_ERR_INCOMPATIBLE, "MM_TENSOR needs a handle sorted with B");
         if (!(sp->c > 0.0) || !std::isfinite(sp->qom) || !std::isfinite(sp->dt) || !std::isfinite(sp->sigma) ||
@@ -325,6 +325,9 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         mm::Geo geo = mm::make_geo(h->g, h->order);
         if (!geo.periodic_x && !ghost)
             return fail(MM_ERR_INVALID_ARG, "slab grid needs a ghost buffer");
+        const size_t esz = prec == MM_FP64 ? sizeof(double) : sizeof(float);
+        if (prec != MM_FP64 && !geo.periodic_x)
+            return fail(MM_ERR_INCOMPATIBLE, "the TF32 paths support whole-domain grids only in this version");
         cudaStream_t s = (cudaStream_t)stream;
         const int64_t S = (2 * h->order + 1) * (2 * h->order + 1) * (2 * h->order + 1);
         const int64_t rowlen = S * (int64_t)kind;
@@ -332,9 +335,9 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         const int64_t nghost = geo.periodic_x ? 0 : (int64_t)mm_ghost_planes(h->order) * h->g.n[1] * h->g.n[2] * rowlen;
         cudaError_t e = cudaSuccess;
         if (!accumulate) {
-            e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)nout, s);
+            e = cudaMemsetAsync(out, 0, esz * (size_t)nout, s);
             if (!e && nghost)
-                e = cudaMemsetAsync(ghost, 0, sizeof(double) * (size_t)nghost, s);
+                e = cudaMemsetAsync(ghost, 0, esz * (size_t)nghost, s);
             if (e)
                 return cuda_fail(e, "mm_assemble memset");
         }
@@ -349,9 +352,12 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         a.ncomp = (int)kind;
         a.wscale = sp->qom * sp->dt / 2.0 / sp->c;
         a.sigma = sp->sigma;
-        a.out = out;
-        a.ghost = geo.periodic_x ? nullptr : ghost;
-        e = mm::assemble_fp64_enqueue(geo, a, s);
+        a.out = static_cast<double *>(out);
+        a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
+        if (prec == MM_FP64)
+            e = mm::assemble_fp64_enqueue(geo, a, s);
+        else
+            e = mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);
         if (e)
             return cuda_fail(e, "mm_assemble launch");
         return MM_OK;

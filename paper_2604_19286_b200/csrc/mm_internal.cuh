@@ -58,11 +58,14 @@ struct AsmArgs {
     int ncomp;            // 1 | 9
     double wscale;        // omega = wscale * B   (= qom*dt/(2c))
     double sigma;
-    double *out;          // owned rows
+    double *out;          // owned rows (FP64; FP32 for the TF32 paths, reinterpreted)
     double *ghost;        // ghost planes (slab only)
     int *work;            // device work counter, zeroed before the launch
 };
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
+
+// ---- TF32 / 3xTF32 on tcgen05 (mm_assemble_tf32.cu); out/ghost hold FP32 ----------
+cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cudaStream_t s);
 
 // ---- halo (mm_halo.cu) -----------------------------------------------------
 cudaError_t ghost_add_enqueue(double *out, const double *recv, int64_t n, cudaStream_t s);

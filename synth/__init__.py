@@ -75,12 +75,12 @@ def _stream(seed: int, plane: int, salt: int = 0) -> np.random.Generator:
 
 
 def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle: bool = True,
-              lattice: bool = False) -> dict:
+              lattice: bool = False, lattice_den: int | None = None) -> dict:
     """Particles located in the cell slab [x_begin, x_end) x [0,n1) x [0,n2).
 
     Returns dict(pos[np,3], q[np], B[np,3]) as float64 numpy arrays.
     lattice=True draws the dyadic variant: xi in {k/16} (order 1)
-    or {k/4} (order 2), q in {1, 2, -1}, B = 2*omega with omega in
+    or {k/4} (order 2) (lattice_den overrides the denominator), q in {1, 2, -1}, B = 2*omega with omega in
     {0, +-e_i, (+-1,+-1,+-1)} so that every product and partial sum of the
     assembly is exact in FP64.
     """
@@ -108,7 +108,7 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle: 
         rng = _stream(cfg.seed, ix)
         sl = slice(k * per_plane, (k + 1) * per_plane)
         if lattice:
-            den = 16 if cfg.order == 1 else 4
+            den = lattice_den or (16 if cfg.order == 1 else 4)
             xi = rng.integers(0, den, size=(per_plane, 3)).astype(np.float64) / den
             qq = np.array([1.0, 2.0, -1.0])[rng.integers(0, 3, size=per_plane)]
             om = omega_set[rng.integers(0, len(omega_set), size=per_plane)]

@@ -334,3 +334,61 @@ def test_full_size_sampled_planes(name):
         sub = {k: v[sel] for k, v in d.items()}
         ref = run_oracle(n, cfg.order, 9, sub).reshape(n[0], plane, S, 9)
         assert rel_err(out[X], ref[X]) <= TOL, X
+
+
+# ---------------------------------------------- TF32 / 3xTF32 (tcgen05) variant
+def run_gpu_tf32(n, order, kind, d, prec, species=None):
+    m = mm()
+    g = m.Grid(n)
+    dd = to_dev(d)
+    h_ = m.mm_sort_by_cell(g, order, 4, dd["pos"], dd["q"], dd["B"] if kind == 9 else None)
+    out = torch.full(m.out_shape(g, order, kind), float("nan"), dtype=torch.float32, device="cuda")
+    m.mm_assemble(h_, kind, prec, species or m.Species(), out)
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+TOL_TF32 = 2e-3      # north_star (row-normalised)
+TOL_TF32X3 = 2e-5    # split TF32 with FP32 accumulation and FP32 output
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("kind", [9, 1])
+@pytest.mark.parametrize("x3", [False, True])
+def test_tf32_parity(order, kind, x3):
+    m = mm()
+    cfg = synth.Config("t", (8, 7, 9), order, "tensor", 40, seed=5)
+    d = synth.particles(cfg)
+    out = run_gpu_tf32(cfg.n, order, kind, d, m.MM_TF32X3 if x3 else m.MM_TF32)
+    ref = run_oracle(cfg.n, order, kind, d)
+    assert rel_err(out, ref) <= (TOL_TF32X3 if x3 else TOL_TF32)
+
+
+@pytest.mark.parametrize("order,den", [(1, 4), (2, 2)])
+@pytest.mark.parametrize("kind", [9, 1])
+def test_tf32_lattice_bit_exact(order, den, kind):
+    # xi in {k/4} (order 1) or {0, 1/2} (order 2): operands exact in TF32, sums exact in FP32
+    m = mm()
+    cfg = synth.Config("t", (6, 5, 7), order, "tensor", 20, seed=13)
+    d = synth.particles(cfg, lattice=True, lattice_den=den)
+    out = run_gpu_tf32(cfg.n, order, kind, d, m.MM_TF32)
+    ref = run_oracle(cfg.n, order, kind, d)
+    assert (out == ref.astype(np.float32).astype(np.float64)).all()
+
+
+def test_tf32_c3_sampled_planes():
+    m = mm()
+    cfg = synth.config("c3")
+    d = synth.particles(cfg)
+    out = run_gpu_tf32(cfg.n, 2, 9, d, m.MM_TF32)
+    n = cfg.n
+    plane = n[1] * n[2]
+    out = out.reshape(n[0], plane, 125, 9)
+    cx = np.floor(d["pos"][:, 0]).astype(np.int64)
+    X = 33
+    sel = np.zeros(len(cx), dtype=bool)
+    for c in range(X - 3, X + 3):
+        sel |= cx == (c % n[0])
+    sub = {k: v[sel] for k, v in d.items()}
+    ref = run_oracle(n, 2, 9, sub).reshape(n[0], plane, 125, 9)
+    assert rel_err(out[X], ref[X]) <= TOL_TF32
