@@ -191,7 +191,7 @@ struct T32 {
     static constexpr int OFF_PA = OFF_PS + PS_BYTES;
     static constexpr int OFF_PW = OFF_PA + PA_BYTES;
     static constexpr int OFF_ST = OFF_PW + PW_BYTES;
-    static constexpr int OFF_ROWP = OFF_ST + STAGE_BYTES;
+    static constexpr int OFF_ROWP = (OFF_ST + STAGE_BYTES + 15) / 16 * 16;
     static constexpr int OFF_SLOT = OFF_ROWP + 32 * 8;
     static constexpr int OFF_BAR = (OFF_SLOT + NN * NN * 2 + 15) / 16 * 16;
     static constexpr int SMEM = OFF_BAR + 32;
