@@ -183,6 +183,7 @@ def main():
     ap.add_argument("--no-order2", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-tf32", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -221,12 +222,14 @@ def main():
         dd = {k: torch.from_numpy(v).to(dev) for k, v in d.items()}
         return cfg, grid, d, dd
 
-    def measure(name, with_extras):
+    def measure(name, with_extras, prec=None):
+        prec = mm.MM_FP64 if prec is None else prec
+        odt = torch.float64 if prec == mm.MM_FP64 else torch.float32
         cfg, grid, d, dd = setup(name)
         order, kind = cfg.order, cfg.ncomp
         sp = mm.Species(cfg.qom, cfg.dt, cfg.c, cfg.sigma)
-        out = torch.empty(mm.out_shape(grid, order, kind), dtype=torch.float64, device=dev)
-        ghost = torch.empty(mm.ghost_shape(grid, order, kind), dtype=torch.float64, device=dev) \
+        out = torch.empty(mm.out_shape(grid, order, kind), dtype=odt, device=dev)
+        ghost = torch.empty(mm.ghost_shape(grid, order, kind), dtype=odt, device=dev) \
             if mm.is_slab(grid) else None
         plane_elems = grid.n[1] * grid.n[2] * (2 * order + 1) ** 3 * kind
         widths = [cfg.n[0] // world] * world
@@ -238,7 +241,7 @@ def main():
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-            mm.mm_assemble(state["h"], kind, mm.MM_FP64, sp, out, ghost)
+            mm.mm_assemble(state["h"], kind, prec, sp, out, ghost)
             if record:
                 e1.record()
                 ev.append((e0, e1))
@@ -335,6 +338,21 @@ def main():
                           "roofline": {"bound": "tensor", "achieved": a2, "peak": fp64_peak, "unit": "TFLOP/s",
                                        "frac": a2 / fp64_peak, "alg_flops_per_particle": F2}}
         del r2
+    if world == 1 and not args.no_tf32:
+        # TF32 / 3xTF32 variant on tcgen05 (FP32 output), reported separately (north_star)
+        tf = {}
+        for name, order in (("c2", 1), ("c3", 2)):
+            for pname, prec in (("tf32", mm.MM_TF32), ("tf32x3", mm.MM_TF32X3)):
+                r = measure(name, False, prec)
+                f = flops_per_particle(order, 9) if order == 1 else 2 * 768 * 9  # paper TF32 tile plan (3 16x16)
+                tf[f"{name}_{pname}"] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
+                                         "assemble_ms": r["assemble_ms"],
+                                         "assemble_mps": r["np"] / (r["assemble_ms"] / 1e3) / 1e6,
+                                         "hbm_achieved_gbs": r["np"] * (64 + (27 if order == 1 else 125) * 9 * 4 /
+                                                                        synth.ppc_of(r["cfg"])) /
+                                         (r["assemble_ms"] / 1e3) / 1e9}
+                del r
+        line["tf32"] = tf
 
     # ---- end to end through the public API with host buffers (pinned), H2D + D2H in the timed region
     if not args.no_e2e:
