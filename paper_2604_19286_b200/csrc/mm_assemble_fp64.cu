@@ -23,6 +23,8 @@
 //   deposit D staged in shared memory, then FP64 REDs driven by a per-lane
 //           table (node index, slot offset) and node-row pointers broadcast by
 //           warp shuffles, issued in address order (contiguous runs).
+#include <cstdlib>
+
 #include "mm_internal.cuh"
 
 namespace mm {
@@ -628,6 +630,17 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     }
 }
 
+// Optional cap on resident assembly CTAs per SM (MM_ASM_CTAS_PER_SM): leaves room for a
+// concurrently running sort on another stream.
+inline int cta_cap()
+{
+    static const int cap = [] {
+        const char *v = getenv("MM_ASM_CTAS_PER_SM");
+        return v ? atoi(v) : 0;
+    }();
+    return cap;
+}
+
 template <typename K>
 unsigned grid_for(K kernel, int64_t items)
 {
@@ -656,6 +669,8 @@ cudaError_t launch_o1(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     }
     int per_sm = 0, dev = 0, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o1<NC>, WARPS * 32, L::SMEM);
+    if (cta_cap() > 0 && per_sm > cta_cap())
+        per_sm = cta_cap();
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t want = (a.nbins + WARPS - 1) / WARPS;
@@ -680,6 +695,8 @@ cudaError_t launch_o2(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     }
     int per_sm = 0, dev = 0, sms = 148;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o2<NC>, L::THREADS, L::SMEM);
+    if (cta_cap() > 0 && per_sm > cta_cap())
+        per_sm = cta_cap();
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     int64_t want = (a.nbins + L::GPC - 1) / L::GPC;
