@@ -184,7 +184,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true")
-    ap.add_argument("--no-pipeline", action="store_true")
+    ap.add_argument("--pipeline", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -250,11 +250,11 @@ def main():
                 slab.exchange_ghosts(out, ghost, order, plane_elems, rank, world, widths,
                                      add=lambda k, src: mm.mm_ghost_add(grid, order, kind, out, src, k, 1))
 
-        # Pipelined schedule (single GPU): the sort of batch k+1 (memory-bound) runs on the main
-        # stream while the assembly of batch k (FP64-pipe-bound) runs on a second stream; two
-        # handles alternate.  Every batch is still fully sorted and assembled; whole-job
-        # throughput = K batches / elapsed.  --no-pipeline gives the serial sort -> assemble step.
-        pipeline = world == 1 and not args.no_pipeline
+        # Optional pipelined schedule (--pipeline, single GPU): the sort of batch k+1 runs on the
+        # main stream while the assembly of batch k runs on a second stream (two handles).
+        # Measured: no gain (the kernels contend for LSU/issue), so the default
+        # step is the serial sort -> assemble.
+        pipeline = world == 1 and args.pipeline
         s_main = torch.cuda.current_stream()
         s_asm = torch.cuda.Stream() if pipeline else s_main
         hs = [None, None]
