@@ -377,10 +377,19 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
             // bitonic sort of the bin's keys held as (v0 = elem lane, v1 = elem lane + 32)
             int32_t v0 = lane < n ? perm[b + lane] : INT_MAX;
             int32_t v1 = lane + 32 < n ? perm[b + lane + 32] : INT_MAX;
-            if (n <= 32)
-                bitonic_reg<32>(v0, v1, lane);
-            else
-                bitonic_reg<64>(v0, v1, lane);
+            // atomic ranks mostly follow the particle index already (CTAs run roughly in
+            // order): skip the network when the slice is ascending
+            const int32_t nx0 = __shfl_down_sync(0xffffffffu, v0, 1);
+            const int32_t first1 = __shfl_sync(0xffffffffu, v1, 0);
+            const int32_t nx1 = __shfl_down_sync(0xffffffffu, v1, 1);
+            const bool ok0 = lane < 31 ? v0 <= nx0 : v0 <= first1;
+            const bool ok1 = lane < 31 ? v1 <= nx1 : true;
+            if (!__all_sync(0xffffffffu, ok0 && ok1)) {
+                if (n <= 32)
+                    bitonic_reg<32>(v0, v1, lane);
+                else
+                    bitonic_reg<64>(v0, v1, lane);
+            }
             if (lane < n) {
                 perm[b + lane] = v0;
                 if (G.on)
