@@ -175,7 +175,7 @@ struct T32 {
     static constexpr int KS = CH / 8;
     static constexpr int L = 2 * ORDER + 1;
     static constexpr int S = L * L * L;
-    static constexpr int THREADS = 256;
+    static constexpr int THREADS = 128;              // one warpgroup: warp w reads TMEM lanes 32w..32w+31
     static constexpr int TMEM_COLS = HALVES * NP <= 32 ? 32 : 64;
     static constexpr int PARTS = X3 ? 2 : 1;         // hi (+ lo)
     // shared memory (bytes)
@@ -204,7 +204,7 @@ __device__ __forceinline__ uint32_t kmajor_off(int row, int k)
 }
 
 template <int ORDER, int NC, bool X3>
-__global__ void __launch_bounds__(256) k_asm_tf32(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(128) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, double wscale,
                                                   double sigma, float *__restrict__ out, float *__restrict__ ghost)
 {
@@ -374,11 +374,12 @@ __global__ void __launch_bounds__(256) k_asm_tf32(Geo g, const double *__restric
         }
         {
             const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
-            const int cgrp = warp >> 2;        // column half handled by this warp
+            constexpr int NCG = T::THREADS / 128;  // column groups (warps sharing a lane quarter)
+            const int cgrp = warp >> 2;
 #pragma unroll
             for (int h = 0; h < T::HALVES; ++h) {
                 const int row = h * 128 + quarter * 32 + lane;
-                for (int c0 = cgrp * 8; c0 < T::NP; c0 += 16) {
+                for (int c0 = cgrp * 8; c0 < T::NP; c0 += 8 * NCG) {
                     float v[8];
                     tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + h * T::NP + c0, v);
                     if (row < T::ROWS) {
