@@ -424,10 +424,19 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
             return e;
         attr = true;
     }
-    int per_sm = 0, dev = 0, sms = 148;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_tf32<ORDER, NC, X3>, T::THREADS, T::SMEM);
+    int per_sm = 0, dev = 0, sms = 148, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // resident CTAs per SM from smem / threads / registers (the occupancy API reports 1 for
+    // this kernel), then capped by TMEM columns below
+    cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_asm_tf32<ORDER, NC, X3>);
+    per_sm = smem_sm / (T::SMEM + 1024);
+    per_sm = min(per_sm, 2048 / T::THREADS);
+    if (fa.numRegs > 0)
+        per_sm = min(per_sm, 65536 / (fa.numRegs * T::THREADS));
+    per_sm = min(per_sm, 16);
     if (per_sm < 1)
         per_sm = 1;
     if (per_sm * T::TMEM_COLS > 512)
