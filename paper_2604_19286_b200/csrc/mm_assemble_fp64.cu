@@ -371,11 +371,12 @@ struct O2 {
     static constexpr int WPG = NC;                   // warps per group
     static constexpr int GPC = NC == 9 ? 1 : 4;      // groups per CTA
     static constexpr int THREADS = WPG * GPC * 32;
-    static constexpr int CH = 32;                    // particles per chunk
-    static constexpr int WS = 36;                    // weight tile row stride (doubles)
+    static constexpr int CH = 64;                    // particles per chunk (2 per lane in the prep)
+    static constexpr int WS = CH + 4;                // weight tile row stride (doubles; 2 wavefronts/LDS)
     static constexpr int WBUF = 32 * WS;             // one weight tile [32 nodes][WS]
+    static constexpr int RBUF = CH * 8;              // one TMA-staged record chunk (doubles)
     static constexpr int STAGE = 378 * NC;          // upper triangle (a <= b) of the 27x27 block
-    static constexpr int GROUP_DOUBLES = 2 * 256 + 2 * WBUF + STAGE + 32 + 2;  // recs, W, stage, rowp, mbar
+    static constexpr int GROUP_DOUBLES = 2 * RBUF + 2 * WBUF + STAGE + 32 + 2;  // recs, W, stage, rowp, mbar
     static constexpr size_t SMEM = (size_t)GPC * GROUP_DOUBLES * 8 + (730 * 2 + 640) * 2 + 8 * GPC + 32 * GPC;
 };
 
@@ -420,8 +421,8 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
     const int gtid = threadIdx.x - grp * L::WPG * 32;  // thread index inside the group
     constexpr int GT = L::WPG * 32;                     // threads per group
     double *gsm = dsm + grp * L::GROUP_DOUBLES;
-    double *srec = gsm;                        // [2][32 records][8]  (TMA-staged chunks)
-    double *wbuf = gsm + 2 * 256;              // [2][32 nodes][WS]
+    double *srec = gsm;                        // [2][CH records][8]  (TMA-staged chunks)
+    double *wbuf = gsm + 2 * L::RBUF;          // [2][32 nodes][WS]
     double *stage = wbuf + 2 * L::WBUF;        // [378 upper pairs][NC]
     double **rowp = reinterpret_cast<double **>(stage + L::STAGE);  // [27]
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 32);  // [2]
@@ -468,7 +469,8 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
         if (gtid == 0) {
             if (b1 > b0 && q[4] != bin)
-                tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(L::CH, b1 - b0) * 64, &bars[chunk & 1]);
+                tma_load(srec + (chunk & 1) * L::RBUF, rec + 8 * (int64_t)b0, min(L::CH, b1 - b0) * 64,
+                         &bars[chunk & 1]);
             const int tnext = q[0];
             tn0 = tn1 = 0;
             if (tnext < nbins) {  // loads in flight until the last chunk of this bin
@@ -486,37 +488,41 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
             // prep (every warp, lane = particle): s^comp and this warp's W rows, from the
             // TMA-staged record chunk
             mbar_wait(&bars[chunk & 1], (chunk >> 1) & 1);
-            double s_me = 0.0;
-            if (lane < m) {
-                const double *r = srec + (chunk & 1) * 256 + 8 * lane;
-                const double2 ra = *reinterpret_cast<const double2 *>(r);
-                const double2 rb = *reinterpret_cast<const double2 *>(r + 2);
-                const double4 r0 = make_double4(ra.x, ra.y, rb.x, rb.y);
-                if (NC == 9) {
-                    const double2 rc = *reinterpret_cast<const double2 *>(r + 4);
-                    s_me = coeff_one(comp, r0.w, rc.x, rc.y, r[6], wscale, sigma);
-                } else {
-                    s_me = sigma * r0.w;
-                }
-                double wx[3], wy[3], wz[3];
-                weights2(r0.x, wx);
-                weights2(r0.y, wy);
-                weights2(r0.z, wz);
-                // runtime node digits: select instead of indexing (keeps wx/wy/wz in registers)
-                auto sel = [](const double *w, int i) { return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]); };
-                if (NC == 9) {
-                    // warp c owns nodes a = c + 9k: digits (k, c/3, c%3)
-                    const double wyc = sel(wy, comp / 3), wzc = sel(wz, comp % 3);
+            double s_me[L::CH / 32];  // s of particles lane, lane + 32, ...
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int a = comp + 9 * k;
-                        if (a < 32)
-                            wt[a * L::WS + lane] = a < 27 ? (wx[k < 3 ? k : 0] * wyc) * wzc : 0.0;
+            for (int j = 0; j < L::CH / 32; ++j) {
+                const int p = lane + 32 * j;
+                s_me[j] = 0.0;
+                if (p < m) {
+                    const double *r = srec + (chunk & 1) * L::RBUF + 8 * p;
+                    const double2 ra = *reinterpret_cast<const double2 *>(r);
+                    const double2 rb = *reinterpret_cast<const double2 *>(r + 2);
+                    if (NC == 9) {
+                        const double2 rc = *reinterpret_cast<const double2 *>(r + 4);
+                        s_me[j] = coeff_one(comp, rb.y, rc.x, rc.y, r[6], wscale, sigma);
+                    } else {
+                        s_me[j] = sigma * rb.y;
                     }
-                } else {
-                    for (int a = 0; a < 32; ++a)
-                        wt[a * L::WS + lane] =
-                            a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
+                    double wx[3], wy[3], wz[3];
+                    weights2(ra.x, wx);
+                    weights2(ra.y, wy);
+                    weights2(rb.x, wz);
+                    // runtime node digits: select instead of indexing (keeps wx/wy/wz in registers)
+                    auto sel = [](const double *w, int i) { return i == 0 ? w[0] : (i == 1 ? w[1] : w[2]); };
+                    if (NC == 9) {
+                        // warp c owns nodes a = c + 9k: digits (k, c/3, c%3)
+                        const double wyc = sel(wy, comp / 3), wzc = sel(wz, comp % 3);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            const int a = comp + 9 * k;
+                            if (a < 32)
+                                wt[a * L::WS + p] = a < 27 ? (wx[k < 3 ? k : 0] * wyc) * wzc : 0.0;
+                        }
+                    } else {
+                        for (int a = 0; a < 32; ++a)
+                            wt[a * L::WS + p] =
+                                a < 27 ? (sel(wx, a / 9) * sel(wy, (a / 3) % 3)) * sel(wz, a % 3) : 0.0;
+                    }
                 }
             }
             group_sync(GT, 1 + grp);
@@ -533,7 +539,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                     q[4] = q[0];
                 }
                 if (cnt)
-                    tma_load(srec + ((chunk + 1) & 1) * 256, src, cnt * 64, &bars[(chunk + 1) & 1]);
+                    tma_load(srec + ((chunk + 1) & 1) * L::RBUF, src, cnt * 64, &bars[(chunk + 1) & 1]);
             }
             const double *wcol = wt + (lane >> 2) * L::WS + (lane & 3);
             auto batch = [&](int kb) {
@@ -541,7 +547,8 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
                     w[r] = wcol[8 * r * L::WS + kb];
-                const double s = __shfl_sync(0xffffffffu, s_me, kb + (lane & 3));
+                const double s = __shfl_sync(0xffffffffu, (kb & 32) ? s_me[L::CH / 32 - 1] : s_me[0],
+                                             (kb & 31) + (lane & 3));
                 double A[4];
 #pragma unroll
                 for (int r = 0; r < 4; ++r)
