@@ -338,7 +338,11 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                 const double v = sm[i * 32 + lane];
                 const int t = s_tab[i * 32 + lane];
                 double *row = shfl_ptr(myrow, t & 7);
+#ifdef MM_EXPERIMENT_NO_FLUSH
+                if (v == 12345.678)  // diagnostics build: deposit skipped
+#else
                 if (v != 0.0)
+#endif
                     red_add(row + (t >> 3), v);
             }
             __syncwarp();
@@ -623,7 +627,11 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
                 for (int a = 0; a < 27; ++a) {
                     const int ab0 = a * 27 + b0c;
                     const double v = stage[s_tri[ab0 + bzl] * 9 + cl];
+#ifdef MM_EXPERIMENT_NO_FLUSH
+                    if (v == 12345.678)  // diagnostics build: deposit skipped
+#else
                     if (v != 0.0)
+#endif
                         red_add(rowp[a] + s_slot[ab0] * 9 + lane, v);
                 }
             }
