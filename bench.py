@@ -210,7 +210,12 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
 
-    def setup(name):
+    cache = {}
+
+    def setup(name, order_kind=True):
+        key = (name, order_kind)
+        if key in cache:
+            return cache[key]
         base = synth.config(name)
         if world == 1:
             cfg, xb, xe = base, 0, base.n[0]
@@ -218,10 +223,12 @@ def main():
             cfg = synth.Config(base.name + f"-weak{world}", (base.n[0] * world, base.n[1], base.n[2]), base.order,
                                base.kind, base.ppc, seed=base.seed)
             xb, xe = rank * base.n[0], (rank + 1) * base.n[0]
-        d = synth.particles(cfg, xb, xe)
+        d = synth.particles(cfg, xb, xe, shuffle=order_kind)
         grid = mm.Grid(cfg.n, cfg.h, xb, xe)
         dd = {k: torch.from_numpy(v).to(dev) for k, v in d.items()}
-        return cfg, grid, d, dd
+        cache.clear()  # keep one workload resident at a time (device memory)
+        cache[key] = (cfg, grid, d, dd)
+        return cache[key]
 
     def measure(name, with_extras, prec=None):
         prec = mm.MM_FP64 if prec is None else prec
@@ -336,6 +343,23 @@ def main():
         res["grid"], res["out"], res["ghost"], res["sp"], res["state"] = grid, out, ghost, sp, state
         return res
 
+    # sort cost when the input is nearly sorted (the PIC-step regime; 10% of particles swapped)
+    sort_nearly_ms = None
+    if world == 1:
+        cfgn, gridn, dn, ddn = setup("c2", "nearly")
+        hn = None
+        for _ in range(3):
+            hn = mm.mm_sort_by_cell(gridn, 1, 4, ddn["pos"], ddn["q"], ddn["B"], handle=hn)
+        barrier()
+        n0, n1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n0.record()
+        for _ in range(20):
+            hn = mm.mm_sort_by_cell(gridn, 1, 4, ddn["pos"], ddn["q"], ddn["B"], handle=hn)
+        n1.record()
+        barrier()
+        sort_nearly_ms = n0.elapsed_time(n1) / 20
+        mm.mm_free(hn)
+        del hn, dn, ddn
     r1 = measure("c2", True)
     cfg = r1["cfg"]
     ppc = synth.ppc_of(cfg)
@@ -378,6 +402,7 @@ def main():
                           "assemble_alone_ms": r1.get("assemble_alone_ms"),
                           "serial_step_ms": (r1.get("sort_ms") or 0) + (r1.get("assemble_alone_ms") or 0),
                           "sort_ms": r1.get("sort_ms"), "assemble_ms": r1["assemble_ms"],
+                          "sort_nearly_sorted_input_ms": sort_nearly_ms,
                           "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
                           "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6}}
 

@@ -105,6 +105,47 @@ __global__ void k_red(double *buf, int64_t nelem, int per_warp, int contig, uint
     }
 }
 
+// The order-1 assembly's batch loop in isolation: per batch one LDS of w, the 9 s values
+// (LDS.128 pairs), 9 DMUL (A = s w) and 9 DMMA; no prep, no deposit.  Shows what DMMA
+// utilisation the DMUL -> DMMA interleave itself allows.
+__global__ void k_batch(int iters, double *sink)
+{
+    __shared__ __align__(16) double sw[8][8 * 36];
+    __shared__ __align__(16) double ss[8][32 * 10];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int i = lane; i < 8 * 36; i += 32)
+        sw[warp][i] = 1.0 + 1e-3 * i;
+    for (int i = lane; i < 32 * 10; i += 32)
+        ss[warp][i] = 0.5 + 1e-3 * i;
+    __syncwarp();
+    double acc[9][2];
+#pragma unroll
+    for (int c = 0; c < 9; ++c)
+        acc[c][0] = acc[c][1] = 0.0;
+    const double *wrow = sw[warp] + (lane >> 2) * 36 + (lane & 3);
+    const double *srow = ss[warp] + (lane & 3) * 10;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int kb = 0; kb < 32; kb += 4) {
+            const double w = wrow[kb];
+            const double *sp = srow + kb * 10;
+#pragma unroll
+            for (int c = 0; c < 8; c += 2) {
+                const double2 sv = *reinterpret_cast<const double2 *>(sp + c);
+                dmma(acc[c][0], acc[c][1], sv.x * w, w);
+                dmma(acc[c + 1][0], acc[c + 1][1], sv.y * w, w);
+            }
+            dmma(acc[8][0], acc[8][1], sp[8] * w, w);
+        }
+    }
+    double s = 0;
+#pragma unroll
+    for (int c = 0; c < 9; ++c)
+        s += acc[c][0] + acc[c][1];
+    if (s == 12345.678)
+        sink[threadIdx.x] = s;
+}
+
 __global__ void k_copy(const double4 *__restrict__ a, double4 *__restrict__ b, int64_t n)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -157,6 +198,12 @@ float probe_mixed(int blocks, int threads, int iters, double *sink)
 float probe_red(double *buf, int64_t nelem, int blocks, int threads, int per_warp, int contig)
 {
     return timed([&] { k_red<<<blocks, threads>>>(buf, nelem, per_warp, contig, 12345u); });
+}
+
+// DMMA flops = blocks * 8 warps * iters * 8 batches * 9 * 512  (blockDim = 256)
+float probe_batch(int blocks, int iters, double *sink)
+{
+    return timed([&] { k_batch<<<blocks, 256>>>(iters, sink); });
 }
 
 // bytes = 2 * n4 * 32

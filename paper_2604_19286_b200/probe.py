@@ -24,7 +24,7 @@ def main():
     args = ap.parse_args()
     lib = ctypes.CDLL(_build.PROBE_LIB)
     F, P, I, I64 = ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
-    for nm, at in (("probe_dmma", [I, I, I, P]), ("probe_dfma", [I, I, I, P]), ("probe_mixed", [I, I, I, P]),
+    for nm, at in (("probe_batch", [I, I, P]), ("probe_dmma", [I, I, I, P]), ("probe_dfma", [I, I, I, P]), ("probe_mixed", [I, I, I, P]),
                    ("probe_red", [P, I64, I, I, I, I]), ("probe_copy", [P, P, I64])):
         getattr(lib, nm).argtypes = at
         getattr(lib, nm).restype = F
@@ -50,6 +50,12 @@ def main():
         ms_f = lib.probe_dfma(b, threads, it, sp)
         best["mixed_ms_vs_sum"].append({"cfg": [blocks_per_sm, threads], "mixed_ms": ms, "dmma_ms": ms_d,
                                         "dfma_ms": ms_f})
+    res["batch_loop"] = []
+    for bps in (1, 2, 3, 4):
+        b = sms * bps
+        ms = lib.probe_batch(b, 500, sp)
+        fl = b * 8 * 500 * 8 * 9 * 512
+        res["batch_loop"].append({"ctas_per_sm": bps, "dmma_tflops": fl / ms / 1e9})
     res["dmma_tflops"] = best["dmma"]
     res["dfma_tflops"] = best["dfma"]
     res["mixed_tflops"] = best["mixed"]

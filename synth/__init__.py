@@ -74,11 +74,13 @@ def _stream(seed: int, plane: int, salt: int = 0) -> np.random.Generator:
     return np.random.Generator(np.random.Philox(key=(int(seed) << 24) ^ (int(plane) << 2) ^ salt))
 
 
-def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle: bool = True,
+def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle=True,
               lattice: bool = False, lattice_den: int | None = None) -> dict:
     """Particles located in the cell slab [x_begin, x_end) x [0,n1) x [0,n2).
 
-    Returns dict(pos[np,3], q[np], B[np,3]) as float64 numpy arrays.
+    Returns dict(pos[np,3], q[np], B[np,3]) as float64 numpy arrays.  Input order: a uniform
+    random shuffle (shuffle=True, the sort's worst case), cell-sorted (False) or "nearly"
+    sorted (10% of the particles swapped with random partners, the PIC-step regime).
     lattice=True draws the dyadic variant: xi in {k/16} (order 1)
     or {k/4} (order 2) (lattice_den overrides the denominator), q in {1, 2, -1}, B = 2*omega with omega in
     {0, +-e_i, (+-1,+-1,+-1)} so that every product and partial sum of the
@@ -128,7 +130,16 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle: 
         pos[sl] = x
         q[sl] = qq
         B[sl] = bb
-    if shuffle and total > 1:
+    if shuffle == "nearly" and total > 1:
+        # generation order is cell-sorted; a PIC step leaves particles nearly sorted:
+        # swap 10% of them with random partners
+        rng = _stream(cfg.seed, x_begin, salt=2)
+        k = total // 10
+        i, j = rng.integers(0, total, size=k), rng.integers(0, total, size=k)
+        perm = np.arange(total)
+        perm[i], perm[j] = perm[j], perm[i]
+        pos, q, B = pos[perm], q[perm], B[perm]
+    elif shuffle and total > 1:
         perm = _stream(cfg.seed, x_begin, salt=1).permutation(total)
         pos, q, B = pos[perm], q[perm], B[perm]
     return {"pos": np.ascontiguousarray(pos), "q": np.ascontiguousarray(q), "B": np.ascontiguousarray(B)}
