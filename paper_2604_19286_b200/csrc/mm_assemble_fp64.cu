@@ -175,6 +175,28 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity)
 
 constexpr int WARPS = 8;
 
+// ---- diagnostics build (-DMM_EXPERIMENT_TIMERS): per-phase SM cycles of the order-1 kernel
+#ifdef MM_EXPERIMENT_TIMERS
+__device__ unsigned long long g_phase[4];  // 0 TMA wait, 1 prep, 2 batches, 3 deposit/other
+#define MM_TDECL unsigned long long t_acc[4] = {0, 0, 0, 0}, t_last = clock64();
+#define MM_TMARK(k)                                  \
+    do {                                             \
+        unsigned long long t_now = clock64();        \
+        t_acc[(k)] += t_now - t_last;                \
+        t_last = t_now;                              \
+    } while (0)
+#define MM_TFLUSH()                                  \
+    do {                                             \
+        if (lane == 0)                               \
+            for (int k = 0; k < 4; ++k)              \
+                atomicAdd(&g_phase[k], t_acc[k]);    \
+    } while (0)
+#else
+#define MM_TDECL
+#define MM_TMARK(k)
+#define MM_TFLUSH()
+#endif
+
 // ---------------------------------------------------------------- order 1
 // Shared memory per warp (doubles):
 //   sh_w [8 nodes][WS]  node-major, WS = 36: batch reads hit 2 wavefronts (minimum)
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
         nb1 = __ldg(seg_begin + bin + nw + 1);
     }
     uint32_t chunk = 0;  // buffer (chunk & 1), mbarrier parity (chunk >> 1) & 1
+    MM_TDECL
     if (lane == 0 && bin < nbins && b1 > b0)
         tma_load(&s_rec[warp][0][0], rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &s_bar[warp][0]);
     while (bin < nbins) {
@@ -268,7 +291,9 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     tma_load(&s_rec[warp][buf ^ 1][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
                              &s_bar[warp][buf ^ 1]);
             }
+            MM_TMARK(3);
             mbar_wait(&s_bar[warp][buf], (chunk >> 1) & 1u);
+            MM_TMARK(0);
             if (lane < m) {
                 const double *r = &s_rec[warp][buf][8 * lane];
                 const double2 ra = *reinterpret_cast<const double2 *>(r);      // xi_x, xi_y
@@ -292,6 +317,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     sh_w[a * L::WS + lane] = (wx[a >> 2] * wy[(a >> 1) & 1]) * wz[a & 1];
             }
             __syncwarp();
+            MM_TMARK(1);
             const double *wrow = sh_w + (lane >> 2) * L::WS + (lane & 3);
             const double *srow = sh_s + (lane & 3) * L::SS;
             auto batch = [&](int kb) {
@@ -318,7 +344,9 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
                     batch(kb);
             }
             __syncwarp();
+            MM_TMARK(2);
         }
+        MM_TMARK(2);
         if (b1 > b0) {
             // ---- deposit: stage D[a][b][c], then RED in address order via the table
 #pragma unroll
@@ -351,12 +379,14 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
             tma_load(&s_rec[warp][chunk & 1u][0], rec + 8 * (int64_t)nb0, min(32, nb1 - nb0) * 64,
                      &s_bar[warp][chunk & 1u]);
         }
+        MM_TMARK(3);
         bin += nw;
         b0 = nb0;
         b1 = nb1;
         nb0 = nn0;
         nb1 = nn1;
     }
+    MM_TFLUSH();
 }
 
 // ---------------------------------------------------------------- order 2
@@ -743,3 +773,14 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
 }
 
 }  // namespace mm
+
+#ifdef MM_EXPERIMENT_TIMERS
+// diagnostics build only: per-phase SM cycles summed over warps since the last call
+extern "C" int mm_debug_phases(unsigned long long *out4)
+{
+    cudaDeviceSynchronize();
+    cudaMemcpyFromSymbol(out4, mm::g_phase, sizeof(unsigned long long) * 4);
+    unsigned long long z[4] = {0, 0, 0, 0};
+    return (int)cudaMemcpyToSymbol(mm::g_phase, z, sizeof(z));
+}
+#endif
