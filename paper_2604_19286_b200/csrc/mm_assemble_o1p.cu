@@ -120,7 +120,7 @@ struct P1 {
     static constexpr int PSZ = PREP > STAGE ? PREP : STAGE;
     static constexpr int NDEP = 64 * NC / 32;           // deposit elements per lane
     // per warp: R[2][CH*8] records | P[2][PSZ] prep/stage | seg[3][U+1] ints | bar[2]
-    static constexpr int WARP_DOUBLES = 2 * CH * 8 + 2 * PSZ + (3 * (U + 1) + 1) / 2 + 1 + 2;
+    static constexpr int WARP_DOUBLES = (2 * CH * 8 + 2 * PSZ + (3 * (U + 1) + 1) / 2 + 1 + 2 + 15) / 16 * 16;  // 128-B aligned
     static constexpr size_t SMEM = (size_t)W1 * WARP_DOUBLES * 8 + 64 * NC * 4;
 };
 
