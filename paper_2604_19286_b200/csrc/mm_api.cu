@@ -355,13 +355,7 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         a.sigma = sp->sigma;
         a.out = static_cast<double *>(out);
         a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
-        static const bool legacy_o1 = [] {  // MM_O1_KERNEL=simple selects the non-pipelined kernel
-            const char *v = getenv("MM_O1_KERNEL");
-            return v && v[0] == 's';
-        }();
-        if (prec == MM_FP64 && h->order == 1 && !legacy_o1)
-            e = mm::assemble_o1p_enqueue(geo, a, s);
-        else if (prec == MM_FP64)
+        if (prec == MM_FP64)
             e = mm::assemble_fp64_enqueue(geo, a, s);
         else
             e = mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);

@@ -92,18 +92,26 @@ __device__ __forceinline__ void coeff(double q, double Bx, double By, double Bz,
     if (NC == 1) {
         s[0] = sigma * q;
     } else {
-        double o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
-        double d = 1.0 + (o0 * o0 + o1 * o1 + o2 * o2);
-        double f = __ddiv_rn(sigma * q, d);
-        s[0] = f * (1.0 + o0 * o0);
-        s[1] = f * (o0 * o1 + o2);
-        s[2] = f * (o0 * o2 - o1);
-        s[3] = f * (o1 * o0 - o2);
-        s[4] = f * (1.0 + o1 * o1);
-        s[5] = f * (o1 * o2 + o0);
-        s[6] = f * (o2 * o0 + o1);
-        s[7] = f * (o2 * o1 - o0);
-        s[8] = f * (1.0 + o2 * o2);
+        // FP64 SIMT work shares the pipe with the DMMAs, so this is written for few
+        // instructions: f = sigma q / d by a Newton-refined reciprocal, then one FMA per
+        // component with f*omega:  s_ij = (f omega_i) omega_j + f delta_ij + eps_ijk f omega_k
+        const double o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
+        const double d = fma(o0, o0, fma(o1, o1, fma(o2, o2, 1.0)));
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+        r = fma(r, fma(-d, r, 1.0), r);
+        r = fma(r, fma(-d, r, 1.0), r);
+        const double f = (sigma * q) * r;
+        const double f0 = f * o0, f1 = f * o1, f2 = f * o2;
+        s[0] = fma(f0, o0, f);
+        s[1] = fma(f0, o1, f2);
+        s[2] = fma(f0, o2, -f1);
+        s[3] = fma(f1, o0, -f2);
+        s[4] = fma(f1, o1, f);
+        s[5] = fma(f1, o2, f0);
+        s[6] = fma(f2, o0, f1);
+        s[7] = fma(f2, o1, -f0);
+        s[8] = fma(f2, o2, f);
     }
 }
 
@@ -426,20 +434,22 @@ __device__ __forceinline__ void group_sync(int nthreads, int id)
 __device__ __forceinline__ double coeff_one(int c, double q, double Bx, double By, double Bz, double wscale,
                                             double sigma)
 {
+    // same expressions as coeff<9> (Newton-refined reciprocal, one FMA per component)
     const double o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
-    const double d = 1.0 + (o0 * o0 + o1 * o1 + o2 * o2);
-    const double f = __ddiv_rn(sigma * q, d);
-    switch (c) {
-    case 0: return f * (1.0 + o0 * o0);
-    case 1: return f * (o0 * o1 + o2);
-    case 2: return f * (o0 * o2 - o1);
-    case 3: return f * (o1 * o0 - o2);
-    case 4: return f * (1.0 + o1 * o1);
-    case 5: return f * (o1 * o2 + o0);
-    case 6: return f * (o2 * o0 + o1);
-    case 7: return f * (o2 * o1 - o0);
-    default: return f * (1.0 + o2 * o2);
-    }
+    const double d = fma(o0, o0, fma(o1, o1, fma(o2, o2, 1.0)));
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    r = fma(r, fma(-d, r, 1.0), r);
+    r = fma(r, fma(-d, r, 1.0), r);
+    const double f = (sigma * q) * r;
+    const double f0 = f * o0, f1 = f * o1, f2 = f * o2;
+    const int i = c / 3, j = c - 3 * i;
+    const double fi = i == 0 ? f0 : (i == 1 ? f1 : f2);
+    const double oj = j == 0 ? o0 : (j == 1 ? o1 : o2);
+    // f delta_ij + eps_ijk f omega_k
+    const double add = c == 0 || c == 4 || c == 8 ? f
+                       : c == 1 ? f2 : c == 2 ? -f1 : c == 3 ? -f2 : c == 5 ? f0 : c == 6 ? f1 : -f0;
+    return fma(fi, oj, add);
 }
 
 template <int NC>

@@ -63,8 +63,6 @@ struct AsmArgs {
     int *work;            // device work counter, zeroed before the launch
 };
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
-// software-pipelined order-1 kernel (mm_assemble_o1p.cu)
-cudaError_t assemble_o1p_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
 
 // ---- TF32 / 3xTF32 on tcgen05 (mm_assemble_tf32.cu); out/ghost hold FP32 ----------
 cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cudaStream_t s);
