@@ -119,8 +119,8 @@ __device__ __forceinline__ void coeff(double q, double Bx, double By, double Bz,
 // w_k = phi(xi - (b + k)).
 __device__ __forceinline__ void weights1(double xi, double w[2])
 {
-    w[0] = 1.0 - xi;              // phi1(xi)
-    w[1] = 1.0 - fabs(xi - 1.0);  // phi1(xi - 1)
+    w[0] = 1.0 - xi;  // phi1(xi)
+    w[1] = xi;        // phi1(xi - 1) = 1 - |xi - 1| = xi for xi in [0, 1) (up to rounding of 1 - xi)
 }
 
 __device__ __forceinline__ void weights2(double xi, double w[3])
