@@ -343,7 +343,7 @@ def main():
         res["grid"], res["out"], res["ghost"], res["sp"], res["state"] = grid, out, ghost, sp, state
         return res
 
-    # sort cost when the input is nearly sorted (the PIC-step regime; 10% of particles swapped)
+    # sort cost when the input is nearly sorted (the PIC-step regime; a random 10% of the particles permuted)
     sort_nearly_ms = None
     if world == 1:
         cfgn, gridn, dn, ddn = setup("c2", "nearly")

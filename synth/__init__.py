@@ -80,7 +80,7 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle=T
 
     Returns dict(pos[np,3], q[np], B[np,3]) as float64 numpy arrays.  Input order: a uniform
     random shuffle (shuffle=True, the sort's worst case), cell-sorted (False) or "nearly"
-    sorted (10% of the particles swapped with random partners, the PIC-step regime).
+    sorted (a random 10% of the particles permuted among themselves, the PIC-step regime).
     lattice=True draws the dyadic variant: xi in {k/16} (order 1)
     or {k/4} (order 2) (lattice_den overrides the denominator), q in {1, 2, -1}, B = 2*omega with omega in
     {0, +-e_i, (+-1,+-1,+-1)} so that every product and partial sum of the
@@ -132,12 +132,13 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle=T
         B[sl] = bb
     if shuffle == "nearly" and total > 1:
         # generation order is cell-sorted; a PIC step leaves particles nearly sorted:
-        # swap 10% of them with random partners
+        # a random 10% of them are permuted among themselves (a true permutation: every
+        # particle appears exactly once)
         rng = _stream(cfg.seed, x_begin, salt=2)
         k = total // 10
-        i, j = rng.integers(0, total, size=k), rng.integers(0, total, size=k)
+        idx = rng.choice(total, size=k, replace=False)
         perm = np.arange(total)
-        perm[i], perm[j] = perm[j], perm[i]
+        perm[idx] = idx[rng.permutation(k)]
         pos, q, B = pos[perm], q[perm], B[perm]
     elif shuffle and total > 1:
         perm = _stream(cfg.seed, x_begin, salt=1).permutation(total)
