@@ -397,6 +397,199 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
     MM_TFLUSH();
 }
 
+// ------------------------------------------------ order 1, tensor: pair-product GEMM
+// The tensor-product B-spline (eq_shape_bspline) makes W_a W_b a product over the axes
+// of per-axis PAIR products q_mu(a_mu + b_mu):  q(0) = w0 w0, q(1) = w0 w1, q(2) = w1 w1
+// (CIC: w0 = 1 - xi, w1 = xi).  So the 8x8x9 block of a bin is
+//
+//   M^c[a][b] = sum_p s^c_p W_a W_b = sum_p X_p[ux uy] Z_p[uz c]   (u_mu = a_mu + b_mu)
+//   X_p[3 ux + uy] = q_x(ux) q_y(uy)   (9 values),   Z_p[9 uz + c] = q_z(uz) s^c_p   (27)
+//
+// one dense product over particles with 9 x 27 = 243 outputs (instead of 64 x 9), and
+// no per-batch A-element scaling: the operands are the prep's products.  DMMA tiles:
+// m = (ux,uy) (9 -> 2 row tiles), n = (uz,c) (27 -> 4 column tiles), 8 DMMA per batch
+// of 4 particles.  Deposit: M^c[a][b] = stage[X row u(a,b)][Z col u(a,b), c] through a
+// table, REDs in the same address order as the node-tile kernel.
+struct O1T {
+    static constexpr int WARPS = 4;
+    static constexpr int XS = 36;                 // row stride (doubles): 2 wavefronts per batch LDS
+    static constexpr int ROWS = 36;               // 9 X rows + 27 Z rows
+    static constexpr int WARP_DOUBLES = ROWS * XS;  // 1296 (stage of 243 aliases it)
+    static constexpr size_t SMEM = (size_t)WARPS * WARP_DOUBLES * 8 + 576 * 4;
+};
+
+__device__ __forceinline__ bool nonzero_bits(double v)
+{
+    return (__double_as_longlong(v) << 1) != 0;  // integer test: keeps the FP64 pipe free
+}
+
+__global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double *__restrict__ rec,
+                                                             const int32_t *__restrict__ seg_begin, int64_t nbins,
+                                                             double wscale, double sigma, double *__restrict__ out,
+                                                             double *__restrict__ ghost)
+{
+    using L = O1T;
+    extern __shared__ __align__(16) double dsm_o1t[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *xz = dsm_o1t + warp * L::WARP_DOUBLES;
+    double *stage = xz;  // [9][27] after the last batch of a bin
+    int32_t *s_dep = reinterpret_cast<int32_t *>(dsm_o1t + L::WARPS * L::WARP_DOUBLES);
+    const int plane = g.n1 * g.n2;
+
+    // deposit table, element e = (a, b, c) in address order of node a's row:
+    // a (3 bits) | slot*9 + c (8 bits) | stage index (X row * 27 + Z col, 8 bits)
+    for (int e = threadIdx.x; e < 576; e += blockDim.x) {
+        const int a = e / 72, r = e - a * 72, b = r / 9, c = r - b * 9;
+        const int ax = a >> 2, ay = (a >> 1) & 1, az = a & 1, bx = b >> 2, by = (b >> 1) & 1, bz = b & 1;
+        const int slot = (bx - ax + 1) * 9 + (by - ay + 1) * 3 + (bz - az + 1);
+        const int m = 3 * (ax + bx) + (ay + by), n = 9 * (az + bz) + c;
+        s_dep[e] = a | ((slot * 9 + c) << 3) | ((m * 27 + n) << 11);
+    }
+    __syncthreads();
+
+    const int nw = gridDim.x * L::WARPS;
+    int bin = blockIdx.x * L::WARPS + warp;
+    int b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
+    if (bin < nbins) {
+        b0 = __ldg(seg_begin + bin);
+        b1 = __ldg(seg_begin + bin + 1);
+    }
+    if (bin + nw < nbins) {
+        nb0 = __ldg(seg_begin + bin + nw);
+        nb1 = __ldg(seg_begin + bin + nw + 1);
+    }
+    // the lane's record of the current chunk, loaded one chunk ahead
+    double4 ra = make_double4(0, 0, 0, 0), rb = ra;
+    if (bin < nbins && b0 + lane < b1) {
+        ra = ld256(rec + 8 * (int64_t)(b0 + lane));
+        rb = ld256(rec + 8 * (int64_t)(b0 + lane) + 4);
+    }
+    // batch-loop operand addresses: A row (lane>>2) (+8 for lanes 0-3), B rows 9 + 8nt + (lane>>2)
+    const int kq = lane & 3, rq = lane >> 2;
+    const double *xa = xz + rq * L::XS + kq;
+    const double *xa1 = xz + 8 * L::XS + kq;                 // row 8 (lanes 0-3 only)
+    const double *zb = xz + (9 + rq) * L::XS + kq;
+    const bool z3 = rq < 3;                                  // rows 9 + 24 + rq < 36
+    while (bin < nbins) {
+        int nn0 = 0, nn1 = 0;
+        if (bin + 2 * nw < nbins) {
+            nn0 = __ldg(seg_begin + bin + 2 * nw);
+            nn1 = __ldg(seg_begin + bin + 2 * nw + 1);
+        }
+        double acc[8][2];
+#pragma unroll
+        for (int t = 0; t < 8; ++t)
+            acc[t][0] = acc[t][1] = 0.0;
+        for (int base = b0; base < b1; base += 32) {
+            const int m = min(32, b1 - base);
+            const double4 ca = ra, cb = rb;
+            // prefetch the lane's record of the next chunk (this bin, else the next bin)
+            {
+                int64_t p = -1;
+                if (base + 32 < b1) {
+                    if (base + 32 + lane < b1)
+                        p = base + 32 + lane;
+                } else if (bin + nw < nbins && nb0 + lane < nb1) {
+                    p = nb0 + lane;
+                }
+                if (p >= 0) {
+                    ra = ld256(rec + 8 * p);
+                    rb = ld256(rec + 8 * p + 4);
+                }
+            }
+            __syncwarp();  // previous batches / deposit are done with xz
+            if (lane < m) {
+                double s[9];
+                coeff<9>(ca.w, cb.x, cb.y, cb.z, wscale, sigma, s);
+                double qx[3], qy[3], qz[3];
+                {
+                    const double w0 = 1.0 - ca.x, w1 = ca.x;
+                    qx[0] = w0 * w0, qx[1] = w0 * w1, qx[2] = w1 * w1;
+                }
+                {
+                    const double w0 = 1.0 - ca.y, w1 = ca.y;
+                    qy[0] = w0 * w0, qy[1] = w0 * w1, qy[2] = w1 * w1;
+                }
+                {
+                    const double w0 = 1.0 - ca.z, w1 = ca.z;
+                    qz[0] = w0 * w0, qz[1] = w0 * w1, qz[2] = w1 * w1;
+                }
+                double *col = xz + lane;
+#pragma unroll
+                for (int i = 0; i < 3; ++i)
+#pragma unroll
+                    for (int j = 0; j < 3; ++j)
+                        col[(3 * i + j) * L::XS] = qx[i] * qy[j];
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+#pragma unroll
+                    for (int c = 0; c < 9; ++c)
+                        col[(9 + 9 * k + c) * L::XS] = qz[k] * s[c];
+            }
+            __syncwarp();
+            auto batch = [&](int kb) {
+                const double a0 = xa[kb];
+                const double a1 = lane < 4 ? xa1[kb] : 0.0;
+                double bv[4];
+#pragma unroll
+                for (int nt = 0; nt < 3; ++nt)
+                    bv[nt] = zb[8 * nt * L::XS + kb];
+                bv[3] = z3 ? zb[24 * L::XS + kb] : 0.0;
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt) {
+                    dmma(acc[nt][0], acc[nt][1], a0, bv[nt]);
+                    dmma(acc[4 + nt][0], acc[4 + nt][1], a1, bv[nt]);
+                }
+            };
+            if (m == 32) {
+#pragma unroll
+                for (int kb = 0; kb < 32; kb += 4)
+                    batch(kb);
+            } else {
+                for (int kb = 0; kb < m; kb += 4)
+                    batch(kb);
+            }
+        }
+        if (b1 > b0) {
+            __syncwarp();
+            // stage[X row][Z col]: D tile (mt, nt) element (rq, 2kq + v)
+#pragma unroll
+            for (int mt = 0; mt < 2; ++mt)
+#pragma unroll
+                for (int nt = 0; nt < 4; ++nt)
+#pragma unroll
+                    for (int v = 0; v < 2; ++v) {
+                        const int mr = 8 * mt + rq, nc = 8 * nt + 2 * kq + v;
+                        if (mr < 9 && nc < 27)
+                            stage[mr * 27 + nc] = acc[4 * mt + nt][v];
+                    }
+            const int bx = bin / plane, rem = bin - bx * plane;
+            const int by = rem / g.n2, bz = rem - by * g.n2;
+            const int a8 = lane & 7;
+            double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
+                                    wrapi(bz + (a8 & 1), g.n2), out, ghost, 27 * 9);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 18; ++i) {
+                const int t = s_dep[i * 32 + lane];
+                const double v = stage[t >> 11];
+                double *row = shfl_ptr(myrow, t & 7);
+                if (nonzero_bits(v))
+                    red_add(row + ((t >> 3) & 255), v);
+            }
+        } else if (bin + nw < nbins && nb0 + lane < nb1) {
+            // empty bin: nothing was prefetched for the successor yet
+            ra = ld256(rec + 8 * (int64_t)(nb0 + lane));
+            rb = ld256(rec + 8 * (int64_t)(nb0 + lane) + 4);
+        }
+        bin += nw;
+        b0 = nb0;
+        b1 = nb1;
+        nb0 = nn0;
+        nb1 = nn1;
+    }
+}
+
 // ---------------------------------------------------------------- order 2
 // 27-node support padded to 32 = 4 row blocks of 8; the 10 upper 8x8 tiles
 // (r <= c) per component (spatial symmetry, eq_spatial_symmetry); the lower
@@ -737,6 +930,42 @@ cudaError_t launch_o1(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     return cudaGetLastError();
 }
 
+cudaError_t launch_o1t(const Geo &geo, const AsmArgs &a, cudaStream_t s)
+{
+    using L = O1T;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_asm_o1t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        if (e)
+            return e;
+        attr = true;
+    }
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o1t, L::WARPS * 32, L::SMEM);
+    if (cta_cap() > 0 && per_sm > cta_cap())
+        per_sm = cta_cap();
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (a.nbins + L::WARPS - 1) / L::WARPS;
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+    k_asm_o1t<<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
+                                                   a.ghost);
+    count_launch();
+    return cudaGetLastError();
+}
+
+// MM_ASM_LEGACY=1 selects the node-tile kernels (A = W s, B = W^T per component) for the
+// tensor kind, for A/B measurements against the pair-product kernels.
+inline bool legacy_tiles()
+{
+    static const bool v = [] {
+        const char *e = getenv("MM_ASM_LEGACY");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 template <int NC>
 cudaError_t launch_o2(const Geo &geo, const AsmArgs &a, cudaStream_t s)
 {
@@ -771,7 +1000,7 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
         return cudaSuccess;
     if (geo.order == 1) {
         if (a.ncomp == 9)
-            return launch_o1<9>(geo, a, s);
+            return legacy_tiles() ? launch_o1<9>(geo, a, s) : launch_o1t(geo, a, s);
         return launch_o1<1>(geo, a, s);
     } else {
         if (a.ncomp == 9)
