@@ -56,6 +56,15 @@ __device__ __forceinline__ void red_add(double *p, double v)
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// v != +-0 as an integer test on the two 32-bit halves: a DSETP would occupy the FP64
+// pipe that the DMMAs need (ptxas turns a 64-bit integer compare of the bits back into one).
+__device__ __forceinline__ bool nonzero_bits(double v)
+{
+    unsigned lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(v));
+    return (lo | (hi << 1)) != 0u;
+}
+
 __device__ __forceinline__ int wrapi(int i, int n)
 {
     return i < 0 ? i + n : (i >= n ? i - n : i);
@@ -377,7 +386,7 @@ __global__ void __launch_bounds__(WARPS * 32, 3) k_asm_o1(Geo g, const double *_
 #ifdef MM_EXPERIMENT_NO_FLUSH
                 if (v == 12345.678)  // diagnostics build: deposit skipped
 #else
-                if (v != 0.0)
+                if (nonzero_bits(v))
 #endif
                     red_add(row + (t >> 3), v);
             }
@@ -417,11 +426,6 @@ struct O1T {
     static constexpr int WARP_DOUBLES = ROWS * XS;  // 1296 (stage of 243 aliases it)
     static constexpr size_t SMEM = (size_t)WARPS * WARP_DOUBLES * 8 + 576 * 4;
 };
-
-__device__ __forceinline__ bool nonzero_bits(double v)
-{
-    return (__double_as_longlong(v) << 1) != 0;  // integer test: keeps the FP64 pipe free
-}
 
 __global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double *__restrict__ rec,
                                                              const int32_t *__restrict__ seg_begin, int64_t nbins,
@@ -863,7 +867,7 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
 #ifdef MM_EXPERIMENT_NO_FLUSH
                     if (v == 12345.678)  // diagnostics build: deposit skipped
 #else
-                    if (v != 0.0)
+                    if (nonzero_bits(v))
 #endif
                         red_add(rowp[a] + s_slot[ab0] * 9 + lane, v);
                 }
@@ -871,8 +875,243 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
         } else {
             for (int e = gtid; e < 729; e += GT) {
                 const double v = stage[s_tri[e]];
-                if (v != 0.0)
+                if (nonzero_bits(v))
                     red_add(rowp[e / 27] + s_slot[e], v);
+            }
+        }
+    }
+}
+
+// ------------------------------------------------ order 2, tensor: pair-product GEMM
+// Same factorisation as k_asm_o1t with TSC weights: per axis the 6 unordered pair
+// products q(P(i,j)) = w_i w_j (P = [[0,1,2],[1,3,4],[2,4,5]]), so the 27x27x9 block is
+//
+//   M^c[a][b] = sum_p X_p[6 ux + uy] Z_p[9 uz + c],  u_mu = P(a_mu, b_mu)
+//   X = q_x(ux) q_y(uy)  (36 rows),   Z = q_z(uz) s^c  (54 rows)
+//
+// 36 x 54 = 1944 outputs (vs 10 upper 8x8 tiles x 9 = 5760 MMA entries), 5 x 7 = 35 DMMA
+// per batch of 4 particles.  One CTA = one bin at a time, 5 warps: warp w owns the D row
+// tile w (7 column tiles, 14 accumulator registers).  Prep of a 32-particle chunk is split
+// by rows (warps 0-1: X rows, warps 2-4: Z rows; lane = particle) into a double-buffered
+// operand tile, so one CTA barrier per chunk suffices.  Flush: 243 runs (node a, b_x, b_y)
+// of 27 contiguous doubles (b_z = 0..2 x 9 comps) of node a's row, each a warp-wide RED
+// over values gathered from the stage through a run table.
+struct O2T {
+    static constexpr int WARPS = 5;
+    static constexpr int XS = 36;                          // row stride (doubles)
+    static constexpr int ROWS = 90;                        // 36 X + 54 Z
+    static constexpr int TILE = ROWS * XS;                 // one operand buffer
+    static constexpr int STAGE = 36 * 54;
+    static constexpr int DOUBLES = 2 * TILE + 2 * 256 + STAGE + 28 + 2 + 122 + 4;  // xz, recs, stage, rowp, bars, runs, q
+    static constexpr size_t SMEM = (size_t)DOUBLES * 8;
+};
+
+// TSC weights of one axis (R3, R4) with u = xi - (b + 1) in [-1/2, 1/2):
+// w0 = (1/2 - u)^2 / 2, w1 = 3/4 - u^2, w2 = (1/2 + u)^2 / 2 (same values as weights2).
+__device__ __forceinline__ void weights2u(double xi, double &w0, double &w1, double &w2)
+{
+    unsigned lo, hi;
+    asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(xi));
+    const double u = hi >= 0x3fe00000u ? xi - 1.0 : xi;  // xi >= 1/2 (xi in [0,1)): base 0, else -1
+    const double h = 0.5 - u, k = 0.5 + u;
+    w0 = (0.5 * h) * h;
+    w1 = fma(-u, u, 0.75);
+    w2 = (0.5 * k) * k;
+}
+
+__global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const double *__restrict__ rec,
+                                                                const int32_t *__restrict__ seg_begin,
+                                                                int64_t nbins, double wscale, double sigma,
+                                                                double *__restrict__ out, double *__restrict__ ghost,
+                                                                int *__restrict__ work)
+{
+    using L = O2T;
+    extern __shared__ __align__(16) double dsm_o2t[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *xzb = dsm_o2t;                                  // [2][90][XS]
+    double *srec = xzb + 2 * L::TILE;                       // [2][32 records][8]
+    double *stage = srec + 2 * 256;                         // [36][54]
+    double **rowp = reinterpret_cast<double **>(stage + L::STAGE);               // [27]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 28);        // [2]
+    int32_t *s_run = reinterpret_cast<int32_t *>(stage + L::STAGE + 30);         // [243]
+    int *q = reinterpret_cast<int *>(stage + L::STAGE + 30 + 122);               // cur, tnext, tnext2, issued
+    const int plane = g.n1 * g.n2;
+    constexpr int RL = 125 * 9;
+
+    // run r = (a, bx, by): a | slot(b - a)|_{bz=0} * 9 << 5 | X row * 54 << 16
+    for (int r = threadIdx.x; r < 243; r += blockDim.x) {
+        const int a = r / 9, bxy = r - 9 * a, bx = bxy / 3, by = bxy - 3 * bx;
+        const int ax = a / 9, ay = (a / 3) % 3, az = a % 3;
+        const int slot = (bx - ax + 2) * 25 + (by - ay + 2) * 5 + (0 - az + 2);
+        const int px = ax + bx + (ax && bx);  // P(ax, bx)
+        const int py = ay + by + (ay && by);
+        s_run[r] = a | ((slot * 9) << 5) | (((6 * px + py) * 54) << 16);
+    }
+    if (threadIdx.x == 0) {
+        q[0] = atom_add(work, 1);
+        q[1] = atom_add(work, 1);
+        q[2] = atom_add(work, 1);
+        q[3] = -1;
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+    }
+    // lane's stage column offsets for a run, by a_z: 9 P(az, bz) + c with l = 9 bz + c
+    const int lbz = lane / 9, lc = lane - 9 * lbz;
+    const int noff0 = 9 * lbz + lc;                                    // P(0, bz) = bz
+    const int noff1 = 9 * (lbz + 1 + (lbz > 0)) + lc;                  // P(1, bz) = 1, 3, 4
+    const int noff2 = 9 * (lbz == 0 ? 2 : lbz + 3) + lc;               // P(2, bz) = 2, 4, 5
+    const int kq = lane & 3, rq = lane >> 2;
+    const bool arow_ok = 8 * warp + rq < 36;
+    const bool b6_ok = rq < 6;  // column tile 6: Z rows 48 + rq < 54
+    __syncthreads();
+    int bin = q[0];
+    int chunk = 0;
+    int tn0 = 0, tn1 = 0;  // (thread 0) range of the next bin
+    while (bin < nbins) {
+        const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
+        if (threadIdx.x == 0) {
+            if (b1 > b0 && q[3] != bin)
+                tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &bars[chunk & 1]);
+            tn0 = tn1 = 0;
+            if (q[1] < nbins) {
+                tn0 = seg_begin[q[1]];
+                tn1 = seg_begin[q[1] + 1];
+            }
+        }
+        double acc[7][2];
+#pragma unroll
+        for (int t = 0; t < 7; ++t)
+            acc[t][0] = acc[t][1] = 0.0;
+        for (int base = b0; base < b1; base += 32, ++chunk) {
+            const int m = min(32, b1 - base);
+            double *xz = xzb + (chunk & 1) * L::TILE;
+            mbar_wait(&bars[chunk & 1], (chunk >> 1) & 1);
+            if (lane < m) {
+                const double *r = srec + (chunk & 1) * 256 + 8 * lane;
+                double *col = xz + lane;
+                if (warp < 2) {
+                    const double2 xy = *reinterpret_cast<const double2 *>(r);
+                    double x0, x1, x2, y0, y1, y2;
+                    weights2u(xy.x, x0, x1, x2);
+                    weights2u(xy.y, y0, y1, y2);
+                    const double qy[6] = {y0 * y0, y0 * y1, y0 * y2, y1 * y1, y1 * y2, y2 * y2};
+                    // warp 0: ux = P(0,0), P(0,1), P(0,2); warp 1: P(1,1), P(1,2), P(2,2)
+                    const double qa = warp == 0 ? x0 : x1;
+                    double qx[3];
+                    qx[0] = qa * qa;
+                    qx[1] = qa * (warp == 0 ? x1 : x2);
+                    qx[2] = (warp == 0 ? x0 : x2) * x2;
+                    double *dst = col + 18 * warp * L::XS;
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+#pragma unroll
+                        for (int j = 0; j < 6; ++j)
+                            dst[(6 * i + j) * L::XS] = qx[i] * qy[j];
+                } else {
+                    const double2 zq = *reinterpret_cast<const double2 *>(r + 2);
+                    const double2 bxy = *reinterpret_cast<const double2 *>(r + 4);
+                    double s[9];
+                    coeff<9>(zq.y, bxy.x, bxy.y, r[6], wscale, sigma, s);
+                    double z0, z1, z2;
+                    weights2u(zq.x, z0, z1, z2);
+                    // warp 2: uz = P(0,0), P(0,1); warp 3: P(0,2), P(1,1); warp 4: P(1,2), P(2,2)
+                    const double za = warp == 2 ? z0 * z0 : (warp == 3 ? z0 * z2 : z1 * z2);
+                    const double zb = warp == 2 ? z0 * z1 : (warp == 3 ? z1 * z1 : z2 * z2);
+                    double *dst = col + (36 + 18 * (warp - 2)) * L::XS;
+#pragma unroll
+                    for (int c = 0; c < 9; ++c) {
+                        dst[c * L::XS] = za * s[c];
+                        dst[(9 + c) * L::XS] = zb * s[c];
+                    }
+                }
+            }
+            __syncthreads();
+            // every warp is past its reads of the other record buffer: prefetch the next chunk
+            if (threadIdx.x == 0) {
+                const double *src = nullptr;
+                int cnt = 0;
+                if (base + 32 < b1) {
+                    src = rec + 8 * (int64_t)(base + 32);
+                    cnt = min(32, b1 - base - 32);
+                } else if (q[1] < nbins && tn1 > tn0) {
+                    src = rec + 8 * (int64_t)tn0;
+                    cnt = min(32, tn1 - tn0);
+                    q[3] = q[1];
+                }
+                if (cnt)
+                    tma_load(srec + ((chunk + 1) & 1) * 256, src, cnt * 64, &bars[(chunk + 1) & 1]);
+            }
+            const double *pa = xz + (8 * warp + rq) * L::XS + kq;
+            const double *pb = xz + (36 + rq) * L::XS + kq;
+            auto batch = [&](int kb) {
+                const double av = arow_ok ? pa[kb] : 0.0;
+                double bv[7];
+#pragma unroll
+                for (int nt = 0; nt < 6; ++nt)
+                    bv[nt] = pb[8 * nt * L::XS + kb];
+                bv[6] = b6_ok ? pb[48 * L::XS + kb] : 0.0;
+#pragma unroll
+                for (int nt = 0; nt < 7; ++nt)
+                    dmma(acc[nt][0], acc[nt][1], av, bv[nt]);
+            };
+            if (m == 32) {
+#pragma unroll
+                for (int kb = 0; kb < 32; kb += 4)
+                    batch(kb);
+            } else {
+                for (int kb = 0; kb < m; kb += 4)
+                    batch(kb);
+            }
+        }
+        if (b0 == b1) {  // empty bin (rare): advance the ticket queue
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                q[0] = q[1];
+                q[1] = q[2];
+                if (q[2] < nbins)
+                    q[2] = atom_add(work, 1);
+            }
+            __syncthreads();
+            bin = q[0];
+            continue;
+        }
+        // ---- stage[X row][Z col]
+        {
+            const int mr = 8 * warp + rq;
+#pragma unroll
+            for (int nt = 0; nt < 7; ++nt)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int nc = 8 * nt + 2 * kq + v;
+                    if (mr < 36 && nc < 54)
+                        stage[mr * 54 + nc] = acc[nt][v];
+                }
+        }
+        const int bx = (int)(bin / plane), rem = bin - bx * plane;
+        const int by = rem / g.n2, bz = rem - by * g.n2;
+        if (threadIdx.x < 27) {
+            const int a = threadIdx.x;
+            rowp[a] = row_ptr(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1), wrapi(bz + a % 3, g.n2),
+                              out, ghost, RL);
+        }
+        if (threadIdx.x == 0) {
+            q[0] = q[1];
+            q[1] = q[2];
+            if (q[2] < nbins)
+                q[2] = atom_add(work, 1);
+        }
+        __syncthreads();
+        bin = q[0];
+        // ---- flush: runs of 27 contiguous doubles in address order of node a's row.  The next
+        //      writes of stage / rowp / q come after the next chunk barrier.
+        if (lane < 27) {
+            for (int r = warp; r < 243; r += L::WARPS) {
+                const int t = s_run[r];
+                const int a = t & 31, az = a - 3 * (a / 3);
+                const double v = stage[(t >> 16) + (az == 0 ? noff0 : (az == 1 ? noff1 : noff2))];
+                if (nonzero_bits(v))
+                    red_add(rowp[a] + ((t >> 5) & 2047) + lane, v);
             }
         }
     }
@@ -925,6 +1164,30 @@ cudaError_t launch_o1(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
     k_asm_o1<NC><<<grid, WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
+                                                   a.ghost, a.work);
+    count_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t launch_o2t(const Geo &geo, const AsmArgs &a, cudaStream_t s)
+{
+    using L = O2T;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_asm_o2t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        if (e)
+            return e;
+        attr = true;
+    }
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_o2t, L::WARPS * 32, L::SMEM);
+    if (cta_cap() > 0 && per_sm > cta_cap())
+        per_sm = cta_cap();
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    unsigned grid = (unsigned)(a.nbins < cap ? (a.nbins < 1 ? 1 : a.nbins) : cap);
+    k_asm_o2t<<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
                                                    a.ghost, a.work);
     count_launch();
     return cudaGetLastError();
@@ -1004,7 +1267,7 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
         return launch_o1<1>(geo, a, s);
     } else {
         if (a.ncomp == 9)
-            return launch_o2<9>(geo, a, s);
+            return legacy_tiles() ? launch_o2<9>(geo, a, s) : launch_o2t(geo, a, s);
         return launch_o2<1>(geo, a, s);
     }
     count_launch();
