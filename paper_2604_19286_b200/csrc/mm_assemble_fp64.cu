@@ -578,8 +578,7 @@ __global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double
                 const int t = s_dep[i * 32 + lane];
                 const double v = stage[t >> 11];
                 double *row = shfl_ptr(myrow, t & 7);
-                if (nonzero_bits(v))
-                    red_add(row + ((t >> 3) & 255), v);
+                red_add(row + ((t >> 3) & 255), v);  // unconditional (+0 contributions are harmless)
             }
         } else if (bin + nw < nbins && nb0 + lane < nb1) {
             // empty bin: nothing was prefetched for the successor yet
@@ -895,14 +894,14 @@ __global__ void __launch_bounds__(O2<NC>::THREADS, NC == 9 ? 3 : 2) k_asm_o2(Geo
 // by rows (warps 0-1: X rows, warps 2-4: Z rows; lane = particle) into a double-buffered
 // operand tile, so one CTA barrier per chunk suffices.  Flush: 243 runs (node a, b_x, b_y)
 // of 27 contiguous doubles (b_z = 0..2 x 9 comps) of node a's row, each a warp-wide RED
-// over values gathered from the stage through a run table.
+// over values gathered from the stage, three runs per table entry (a, b_x).
 struct O2T {
     static constexpr int WARPS = 5;
     static constexpr int XS = 36;                          // row stride (doubles)
     static constexpr int ROWS = 90;                        // 36 X + 54 Z
     static constexpr int TILE = ROWS * XS;                 // one operand buffer
     static constexpr int STAGE = 36 * 54;
-    static constexpr int DOUBLES = 2 * TILE + 2 * 256 + STAGE + 28 + 2 + 122 + 4;  // xz, recs, stage, rowp, bars, runs, q
+    static constexpr int DOUBLES = 2 * TILE + 2 * 256 + STAGE + 28 + 2 + 162 + 4;  // xz, recs, stage, rowp, bars, units, q
     static constexpr size_t SMEM = (size_t)DOUBLES * 8;
 };
 
@@ -933,19 +932,22 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
     double *stage = srec + 2 * 256;                         // [36][54]
     double **rowp = reinterpret_cast<double **>(stage + L::STAGE);               // [27]
     uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 28);        // [2]
-    int32_t *s_run = reinterpret_cast<int32_t *>(stage + L::STAGE + 30);         // [243]
-    int *q = reinterpret_cast<int *>(stage + L::STAGE + 30 + 122);               // cur, tnext, tnext2, issued
+    int4 *s_unit = reinterpret_cast<int4 *>(stage + L::STAGE + 30);             // [81]
+    int *q = reinterpret_cast<int *>(stage + L::STAGE + 30 + 162);               // cur, tnext, tnext2, issued
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * 9;
 
-    // run r = (a, bx, by): a | slot(b - a)|_{bz=0} * 9 << 5 | X row * 54 << 16
-    for (int r = threadIdx.x; r < 243; r += blockDim.x) {
-        const int a = r / 9, bxy = r - 9 * a, bx = bxy / 3, by = bxy - 3 * bx;
+    // flush unit u = (a, bx): {a, slot(b - a)*9 at by = bz = 0, stage row offsets 54 X(by) for
+    // by = 0..2 (16-bit fields), a_z}; X(by) = 6 P(ax, bx) + P(ay, by), P(i,j) = i + j + [i,j > 0]
+    for (int u = threadIdx.x; u < 81; u += blockDim.x) {
+        const int a = u / 3, bx = u - 3 * a;
         const int ax = a / 9, ay = (a / 3) % 3, az = a % 3;
-        const int slot = (bx - ax + 2) * 25 + (by - ay + 2) * 5 + (0 - az + 2);
-        const int px = ax + bx + (ax && bx);  // P(ax, bx)
-        const int py = ay + by + (ay && by);
-        s_run[r] = a | ((slot * 9) << 5) | (((6 * px + py) * 54) << 16);
+        const int slot = (bx - ax + 2) * 25 + (0 - ay + 2) * 5 + (0 - az + 2);
+        const int px = ax + bx + (ax && bx);
+        int m54[3];
+        for (int by = 0; by < 3; ++by)
+            m54[by] = 54 * (6 * px + ay + by + (ay && by));
+        s_unit[u] = make_int4(a, slot * 9, m54[0] | (m54[1] << 16), m54[2] | (az << 16));
     }
     if (threadIdx.x == 0) {
         q[0] = atom_add(work, 1);
@@ -961,6 +963,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
     const int noff0 = 9 * lbz + lc;                                    // P(0, bz) = bz
     const int noff1 = 9 * (lbz + 1 + (lbz > 0)) + lc;                  // P(1, bz) = 1, 3, 4
     const int noff2 = 9 * (lbz == 0 ? 2 : lbz + 3) + lc;               // P(2, bz) = 2, 4, 5
+    const int d1 = noff1 - noff0, d2 = noff2 - noff0;
     const int kq = lane & 3, rq = lane >> 2;
     const bool arow_ok = 8 * warp + rq < 36;
     const bool b6_ok = rq < 6;  // column tile 6: Z rows 48 + rq < 54
@@ -1103,15 +1106,22 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
         }
         __syncthreads();
         bin = q[0];
-        // ---- flush: runs of 27 contiguous doubles in address order of node a's row.  The next
-        //      writes of stage / rowp / q come after the next chunk barrier.
+        // ---- flush: runs of 27 contiguous doubles (b_z x comps) of node a's row, three runs
+        //      (b_y = 0..2, 5 slots apart) per unit (a, b_x).  The next writes of stage / rowp /
+        //      q come after the next chunk barrier.
         if (lane < 27) {
-            for (int r = warp; r < 243; r += L::WARPS) {
-                const int t = s_run[r];
-                const int a = t & 31, az = a - 3 * (a / 3);
-                const double v = stage[(t >> 16) + (az == 0 ? noff0 : (az == 1 ? noff1 : noff2))];
-                if (nonzero_bits(v))
-                    red_add(rowp[a] + ((t >> 5) & 2047) + lane, v);
+#pragma unroll 2
+            for (int u = warp; u < 81; u += L::WARPS) {
+                const int4 t = s_unit[u];
+                const int az = t.w >> 16;
+                const int no = noff0 + (d1 & -(az == 1)) + (d2 & -(az == 2));
+                double *p = rowp[t.x] + t.y + lane;
+                const double v0 = stage[(t.z & 0xffff) + no];
+                const double v1 = stage[(t.z >> 16) + no];
+                const double v2 = stage[(t.w & 0xffff) + no];
+                red_add(p, v0);  // unconditional: a predicated RED costs a branch (BSSY/BSYNC)
+                red_add(p + 45, v1);
+                red_add(p + 90, v2);
             }
         }
     }
