@@ -37,10 +37,24 @@ UNIT = "Mparticles/s"
 HBM_BYTES_PER_PARTICLE_IN = 56.0   # x,y,z,q,Bx,By,Bz (FP64) read once
 
 
-def flops_per_particle(order, ncomp):
-    # F_method: 2 x (MMA entries per component issued by the tile plan) x C
-    entries = 64 if order == 1 else 640
-    return 2 * entries * ncomp
+def flops_per_particle(order, ncomp, kind="unique"):
+    """FP64 FLOPs per particle:
+    unique   F_unique = 2 x N(N+1)/2 x C, N = 8 | 27 support nodes (the stricter
+             floor): the `roofline` figure
+    plan     F_method = 2 x (MMA entries per component of the paper's tile plan: 64 | 640) x C
+    pair     this build's pair-product contraction: 2 x (9 x 27 | 36 x 54) (tensor)
+    executed DMMA FLOPs issued by the pair-product kernels incl. tile padding: 8 | 35 DMMA.8x8x4
+             per batch of 4 particles"""
+    n = 8 if order == 1 else 27
+    if kind == "unique":
+        return 2 * (n * (n + 1) // 2) * ncomp
+    if kind == "plan":
+        return 2 * (64 if order == 1 else 640) * ncomp
+    if kind == "pair":
+        return 2 * (9 * 27 if order == 1 else 36 * 54) * ncomp // 9
+    if kind == "executed":
+        return (8 if order == 1 else 35) * 512 // 4
+    raise ValueError(kind)
 
 
 def alg_bytes_per_particle(order, ncomp, ppc):
@@ -375,14 +389,25 @@ def main():
         fp64_peak = peaks.get("bf16_tflops", 1590.0) * 40.0 / 2250.0
         fp64_src = f"{peak_src} bf16 x nominal FP64/bf16 ratio 40/2250"
     achieved = r1["np"] * F / (r1["assemble_ms"] / 1e3) / 1e12
+
+    def flop_views(r, order):
+        t = r["assemble_ms"] / 1e3
+        v = {}
+        for k in ("plan", "pair", "executed"):
+            f = flops_per_particle(order, 9, k)
+            v[k] = {"flops_per_particle": f, "tflops": r["np"] * f / t / 1e12, "frac": r["np"] * f / t / 1e12 / fp64_peak}
+        return v
+
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         with open(tp) as f:
             traffic = json.load(f).get("assemble_o1_bytes_per_launch")
-    roof = {"bound": "tensor", "kernel": "mm_assemble (k_asm_o1<9> FP64 DMMA + zero-fill)", "achieved": achieved,
-            "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak, "traffic": traffic,
-            "peak_source": fp64_src, "alg_flops_per_particle": F,
+    roof = {"bound": "tensor", "kernel": "mm_assemble (k_asm_o1t pair-product FP64 DMMA + zero-fill)",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+            "traffic": traffic, "peak_source": fp64_src, "alg_flops_per_particle": F,
+            "alg_flops_definition": "F_unique = 2 x 36 node pairs x 9 comps (SURVEY.md 8(d) stricter floor)",
+            "other_flop_counts": flop_views(r1, 1),
             "alg_bytes_per_particle": alg_bytes_per_particle(1, 9, ppc),
             "hbm_achieved_gbs": r1["np"] * alg_bytes_per_particle(1, 9, ppc) / (r1["assemble_ms"] / 1e3) / 1e9,
             "hbm_peak_gbs": peaks.get("hbm_gbs")}
@@ -414,8 +439,11 @@ def main():
                           "c3 weak-scaled slabs", "value": r2["value"], "unit": UNIT, "ms_per_step": r2["ms_per_step"],
                           "sort_ms": r2.get("sort_ms"), "assemble_ms": r2["assemble_ms"],
                           "assemble_alone_ms": r2.get("assemble_alone_ms"), "pipelined": r2["pipelined"],
-                          "roofline": {"bound": "tensor", "achieved": a2, "peak": fp64_peak, "unit": "TFLOP/s",
-                                       "frac": a2 / fp64_peak, "alg_flops_per_particle": F2}}
+                          "roofline": {"bound": "tensor", "kernel": "mm_assemble (k_asm_o2t + zero-fill)",
+                                       "achieved": a2, "peak": fp64_peak, "unit": "TFLOP/s",
+                                       "frac": a2 / fp64_peak, "alg_flops_per_particle": F2,
+                                       "alg_flops_definition": "F_unique = 2 x 378 node pairs x 9 comps",
+                                       "other_flop_counts": flop_views(r2, 2)}}
         del r2
     if world == 1 and not args.no_tf32:
         # TF32 / 3xTF32 variant on tcgen05 (FP32 output), reported separately (north_star)
@@ -423,7 +451,6 @@ def main():
         for name, order in (("c2", 1), ("c3", 2)):
             for pname, prec in (("tf32", mm.MM_TF32), ("tf32x3", mm.MM_TF32X3)):
                 r = measure(name, False, prec)
-                f = flops_per_particle(order, 9) if order == 1 else 2 * 768 * 9  # paper TF32 tile plan (3 16x16)
                 tf[f"{name}_{pname}"] = {"value": r["value"], "unit": UNIT, "ms_per_step": r["ms_per_step"],
                                          "assemble_ms": r["assemble_ms"],
                                          "assemble_mps": r["np"] / (r["assemble_ms"] / 1e3) / 1e6,

@@ -4,25 +4,25 @@
 //   for each support group (here: a support-window bin, R12)
 //     D^{ij} <- 0                                             (alg. line 399)
 //     for each batch of K_t = 4 particles                     (eq_D_batches)
-//       A^{ij}_{ak} = W_{a p_k} s^{ij}_{p_k},  B_{kb} = W_{b p_k}  (eq_AB_batch)
-//       D^{ij} += A^{ij} B                    one DMMA per tile and component
+//       D^{ij} += A^{ij} B   (dense product over the batch)   (eq_AB_batch)
 //     deposit D^{ij} into the node-stencil storage
 //
-// Fragment mapping of mma.sync.m8n8k4.f64 (row.col): lane t holds
-// A[t>>2][t&3], B[t&3][t>>2] and D[t>>2][2(t&3)+v].  With rows = support
-// nodes and k = particles, lane t needs exactly ONE weight per 8-node block,
-// w = W_{t>>2}(p_{t&3}): it is its B element unscaled and, times s^{ij}, its
-// A element.
+// Two operand plans:
+//  * pair-product (default for the tensor kind; k_asm_o1t, k_asm_o2t): the tensor-product
+//    B-spline makes W_a W_b a product of per-axis pair products, so the block of a bin is
+//    ONE product over particles with X = q_x q_y rows and Z = q_z s^{ij} columns
+//    (9 x 27 | 36 x 54 outputs) -- see the comments at O1T / O2T;
+//  * node tiles (the paper's plan; scalar kind, and MM_ASM_LEGACY=1): rows = support nodes,
+//    A = W s^{ij}, B = W^T per component (one 8x8 tile | 10 upper 8x8 tiles).
 //
-// Structure of both kernels (one warp = one bin [x component group]):
-//   prep    one lane per particle of a chunk: 2 x 256-bit record loads, s^{ij}
-//           (alpha, eq_alpha_matrix) and the tensor-product weights W_a,
-//           staged in shared memory in bank-conflict-free layouts;
-//   batch   per batch of 4 particles: LDS of w and s, one DMUL per A element,
-//           one DMMA per tile and component (accumulators in registers);
-//   deposit D staged in shared memory, then FP64 REDs driven by a per-lane
-//           table (node index, slot offset) and node-row pointers broadcast by
-//           warp shuffles, issued in address order (contiguous runs).
+// Fragment mapping of mma.sync.m8n8k4.f64 (row.col): lane t holds A[t>>2][t&3],
+// B[t&3][t>>2] and D[t>>2][2(t&3)+v]; operands are staged in shared memory with a row
+// stride of 36 doubles (the 8 rows x 4 particles of a fragment load hit 2 wavefronts).
+//
+// Phases of every kernel: prep (one lane per particle of a chunk: s^{ij} from the record
+// (alpha, eq_alpha_matrix) and the weights / products into shared memory), batches (DMMA,
+// accumulators in registers), deposit (D staged in shared memory, FP64 REDs in global
+// address order through a table, node-row pointers broadcast by shuffles).
 #include <cstdlib>
 
 #include "mm_internal.cuh"

@@ -98,9 +98,9 @@ def main():
                 v = float(v.replace(",", ""))
                 return v * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1)
             nm = name.replace("(int)", "").replace(" ", "")
-            if "k_asm_o1<9>" in nm and "dram__bytes_read.sum" in d:
+            if ("k_asm_o1t" in nm or "k_asm_o1<9>" in nm) and "dram__bytes_read.sum" in d:
                 traffic["assemble_o1_bytes_per_launch"] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
-            if "k_asm_o2<9>" in nm and "dram__bytes_read.sum" in d:
+            if ("k_asm_o2t" in nm or "k_asm_o2<9>" in nm) and "dram__bytes_read.sum" in d:
                 traffic["assemble_o2_bytes_per_launch"] = to_bytes("dram__bytes_read.sum") + to_bytes("dram__bytes_write.sum")
     lc = os.path.join(a.src, "launches.csv")
     if os.path.exists(lc):
