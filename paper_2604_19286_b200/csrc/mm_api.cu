@@ -3,6 +3,7 @@
 // mm_sort.cu, mm_assemble_fp64.cu and mm_halo.cu.
 #include <atomic>
 #include <cmath>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -125,6 +126,16 @@ Geo make_geo(const mm_grid &g, int order)
     o.order = order;
     o.periodic_x = (g.x_begin == 0 && g.x_end == g.n[0]) ? 1 : 0;
     o.nbx = g.x_end - g.x_begin + order - 1;
+    // Division by a power of two is the exact product with its (exact) reciprocal, so the
+    // IEEE-RN quotient x/h equals RN(x * (1/h)) bit for bit (R5).
+    auto pow2 = [](double h) {
+        int ex;
+        return std::frexp(h, &ex) == 0.5 && ex > -1000 && ex < 1000;
+    };
+    o.ih0 = 1.0 / g.h[0];
+    o.ih1 = 1.0 / g.h[1];
+    o.ih2 = 1.0 / g.h[2];
+    o.h_pow2 = pow2(g.h[0]) && pow2(g.h[1]) && pow2(g.h[2]);
     return o;
 }
 

@@ -16,6 +16,8 @@ struct Geo {
     int order;
     int periodic_x;  // whole axis 0 owned -> wrap, else slab with ghost planes
     int nbx;         // bins along axis 0 = x_end - x_begin + order - 1
+    double ih0, ih1, ih2;  // 1/h, exact when the spacing is a power of two
+    int h_pow2;            // all three spacings powers of two: x/h == x * (1/h) bit for bit
 };
 
 Geo make_geo(const mm_grid &g, int order);

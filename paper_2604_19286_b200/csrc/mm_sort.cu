@@ -16,6 +16,7 @@
 //              write pad slots; warp path (<= 1024), CTA path (<= 16384), huge path
 //   k_scatter  coalesced over particles: rec[dest[p]] = {xi, q, B, 0} (64-B records)
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 
 #include "mm_internal.cuh"
@@ -41,6 +42,7 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
     L.err = 0;
     const double x[3] = {x0, x1, x2};
     const double h[3] = {g.h0, g.h1, g.h2};
+    const double ih[3] = {g.ih0, g.ih1, g.ih2};
 #pragma unroll
     for (int mu = 0; mu < 3; ++mu) {
         if (!isfinite(x[mu])) {
@@ -49,7 +51,9 @@ __device__ __forceinline__ Located locate(const Geo &g, double x0, double x1, do
             L.c[mu] = 0;
             continue;
         }
-        double u = __ddiv_rn(x[mu], h[mu]);  // IEEE RN division (bit-exact binning)
+        // IEEE RN division (bit-exact binning); for a power-of-two spacing the product with
+        // the exact reciprocal is the same correctly rounded quotient
+        double u = g.h_pow2 ? x[mu] * ih[mu] : __ddiv_rn(x[mu], h[mu]);
         double c = floor(u);
         L.xi[mu] = u - c;
         double lo = mu == 0 ? (double)g.x_begin : 0.0;
@@ -280,7 +284,11 @@ constexpr int FIX_WARPS = 8;
 
 __device__ __forceinline__ void st256(double *p, double a, double b, double c, double d)
 {
+#ifdef MM_SCATTER_CS
+    asm volatile("st.global.cs.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+#else
     asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+#endif
 }
 
 
@@ -577,6 +585,47 @@ inline unsigned blocks_for(int64_t n, int t)
     return (unsigned)((n + t - 1) / t);
 }
 
+// Diagnostics (MM_SORT_TIMERS=1): CUDA events after every phase, printed to stderr.
+struct PhaseTimer {
+    bool on = false;
+    cudaStream_t s = nullptr;
+    int n = 0;
+    cudaEvent_t ev[32];
+    const char *tag[32];
+    explicit PhaseTimer(cudaStream_t st) : s(st)
+    {
+        static const bool env = [] {
+            const char *v = getenv("MM_SORT_TIMERS");
+            return v && v[0] == '1';
+        }();
+        on = env;
+        mark("start");
+    }
+    void mark(const char *t)
+    {
+        if (!on || n >= 32)
+            return;
+        cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], s);
+        tag[n++] = t;
+    }
+    ~PhaseTimer()
+    {
+        if (!on)
+            return;
+        cudaEventSynchronize(ev[n - 1]);
+        fprintf(stderr, "[mm sort]");
+        for (int i = 1; i < n; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            fprintf(stderr, " %s %.1f", tag[i], ms * 1e3f);
+        }
+        fprintf(stderr, " us\n");
+        for (int i = 0; i < n; ++i)
+            cudaEventDestroy(ev[i]);
+    }
+};
+
 }  // namespace
 
 int64_t scan_tmp_elems(int64_t nbins)
@@ -587,6 +636,7 @@ int64_t scan_tmp_elems(int64_t nbins)
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
 {
     cudaError_t e;
+    PhaseTimer pt(s);
     if ((e = cudaMemsetAsync(b.count, 0, sizeof(int32_t) * (size_t)b.nbins, s)))
         return e;
     if ((e = cudaMemsetAsync(b.status, 0, sizeof(int32_t) * ST_WORDS, s)))
@@ -606,15 +656,18 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         else
             k_key<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
         count_launch();
+        pt.mark("key");
     }
     const int nblk = (int)((b.nbins + SCAN_TILE - 1) / SCAN_TILE);
     k_scan_local<<<nblk, SCAN_T, 0, s>>>(b.count, b.nbins, b.k_pad, b.seg_begin, b.scan_tmp);
     k_scan_top<<<1, SCAN_T, 0, s>>>(b.scan_tmp, nblk, b.seg_begin + b.nbins, b.status);
     k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
     count_launch(3);
+    pt.mark("scan");
     if (b.np > 0) {
         k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
         count_launch();
+        pt.mark("place");
     }
     {
         int64_t want = (b.nbins + FIX_WARPS - 1) / FIX_WARPS;
@@ -624,6 +677,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         k_fix_warp<<<grid, FIX_WARPS * 32, 0, s>>>(b.nbins, b.count, b.seg_begin, b.perm, b.rank, b.rec,
                                                    b.mid_list, b.huge_list, b.status, G);
         count_launch();
+        pt.mark("fix");
     }
     if (b.np > WARP_BIN_MAX) {
         static bool attr = false;
@@ -648,6 +702,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
             k_scatter<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
                                                                        b.rec, b.status);
         count_launch();
+        pt.mark("scatter");
     }
     return cudaGetLastError();
 }
