@@ -1,20 +1,28 @@
 // TF32 / 3xTF32 variant of the assembly on the 5th-generation tensor cores
-// (tcgen05.mma kind::tf32, accumulators in TMEM), "reported separately" from the
+// (tcgen05.mma kind::tf32, FP32 accumulators in TMEM), "reported separately" from the
 // FP64 DMMA path (north_star; PAPER.md:186 reduced-precision inputs with wider
 // accumulation, PAPER.md:431 TF32 inputs / FP32 accumulation).
 //
-// Mapping (one CTA = one support-window bin at a time, Algorithm 1):
-//   rows    m = c*NN + a   (component c, support node a)  -> M = 128 per MMA (HALVES of them)
-//   columns n = b          (support node b, padded to NP) -> N = NP (8 or 32)
-//   K       8 particles per tcgen05.mma (32 B of TF32)
-//   A[m][k] = tf32(s_c(p_k) W_a(p_k)),  B[n][k] = tf32(W_b(p_k))      (eq_AB_batch)
-//   D[m][n] += A B^T in TMEM (FP32)                                    (eq_mma_accumulate)
-// 3xTF32: x = hi + lo with hi = rna(x), lo = rna(x - hi); D += Ah Bh + Ah Bl + Al Bh.
-// Operands are built by the CTA's threads in shared memory in the UMMA K-major
-// no-swizzle canonical layout (8-row x 16-B core matrices; LBO = 128 B between the two
-// K halves, SBO = 256 B between 8-row groups) and consumed by one elected thread's MMA.
-// The epilogue reads TMEM with tcgen05.ld, stages the block in shared memory and
-// flushes FP32 REDs in global address order (output FP32, R17).
+// Operand plan: the pair-product factorisation of the FP64 kernels (mm_assemble_fp64.cu,
+// O1T / O2T): per bin (support group, Algorithm 1)
+//
+//   M^c[a][b] = sum_p X_p[ux uy] Z_p[uz c],  X = q_x q_y (NX = 9 | 36),  Z = q_z s^c (NZ = 3C | 6C)
+//
+// with q_mu the per-axis pair products of the B-spline weights (u_mu = a_mu + b_mu for CIC,
+// the unordered pair index for TSC).  One tcgen05.mma (M = 128, K = 8 particles) covers BPC
+// bins at once: bin j owns A rows [MB j, MB j + NZ) (A = Z, MB = 128 / BPC) and B rows
+// [NB j, NB j + NX) (B = X), so D[MB j + z][NB j + x] is bin j's block; the off-diagonal
+// blocks of D are unused.  The tensor work is tiny next to the HBM traffic, so the wasted
+// blocks cost nothing measurable, and the layout puts bin j's rows in TMEM lanes that its
+// own warp(s) can read (tcgen05.ld: warp w reads lanes 32 (w % 4) .. +31).
+//   order 1: BPC = 4, MB = 32, NB = 16, N = 64   (warp j = bin j)
+//   order 2: BPC = 2, MB = 64, NB = 64, N = 128  (warps 2j, 2j+1 = bin j: X / Z prep, lane halves)
+// Per 32-particle chunk: prep (FP32 from the FP64 record; the support base is decided in FP64
+// exactly as in the sort) -> staging [row][particle] -> TF32 (cvt.rna) K-major tiles (no-swizzle
+// canonical layout: 8-row x 16-B core matrices, LBO = 128 B, SBO = 256 B) in a double buffer ->
+// one thread issues 4 K-steps (x3 for 3xTF32: D += Ah Bh + Ah Bl + Al Bh) and commits to the
+// buffer's mbarrier.  Epilogue per group: tcgen05.ld -> staged block -> FP32 REDs in global
+// address order (the FP64 kernels' deposit tables).
 #include "mm_internal.cuh"
 
 namespace mm {
@@ -112,130 +120,161 @@ __device__ __forceinline__ void tc_fence_after()
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
 
-// 32 lanes x 8 consecutive 32-bit TMEM columns -> registers (one row per thread).
-__device__ __forceinline__ void tmem_ld8(uint32_t taddr, float v[8])
+
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16])
 {
-    uint32_t r[8];
-    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                   "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]),
+                   "=r"(r[15])
                  : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < 16; ++i)
         v[i] = __uint_as_float(r[i]);
 }
 
-// ---- per-particle coefficients / weights (same expressions as the FP64 path) ---
-template <int NC>
-__device__ __forceinline__ void coeff(double q, double Bx, double By, double Bz, double wscale, double sigma,
-                                      double s[NC])
+__device__ __forceinline__ void tmem_wait_ld()
 {
-    if (NC == 1) {
-        s[0] = sigma * q;
-    } else {
-        double o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
-        double d = 1.0 + (o0 * o0 + o1 * o1 + o2 * o2);
-        double f = __ddiv_rn(sigma * q, d);
-        s[0] = f * (1.0 + o0 * o0);
-        s[1] = f * (o0 * o1 + o2);
-        s[2] = f * (o0 * o2 - o1);
-        s[3] = f * (o1 * o0 - o2);
-        s[4] = f * (1.0 + o1 * o1);
-        s[5] = f * (o1 * o2 + o0);
-        s[6] = f * (o2 * o0 + o1);
-        s[7] = f * (o2 * o1 - o0);
-        s[8] = f * (1.0 + o2 * o2);
-    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int ORDER>
-__device__ __forceinline__ void axis_weights(double xi, double w[3])
-{
-    if (ORDER == 1) {
-        w[0] = 1.0 - xi;
-        w[1] = 1.0 - fabs(xi - 1.0);
-        w[2] = 0.0;
-    } else {
-        double b = xi >= 0.5 ? 0.0 : -1.0;
-        double t0 = fabs(xi - b), t1 = xi - (b + 1.0), t2 = fabs(xi - (b + 2.0));
-        w[0] = 0.5 * (1.5 - t0) * (1.5 - t0);
-        w[1] = 0.75 - t1 * t1;
-        w[2] = 0.5 * (1.5 - t2) * (1.5 - t2);
-    }
-}
-
-template <int ORDER, int NC, bool X3>
-struct T32 {
-    static constexpr int N1 = ORDER + 1;
-    static constexpr int NN = N1 * N1 * N1;          // support nodes: 8 | 27
-    static constexpr int NP = ORDER == 1 ? 8 : 32;   // MMA N (nodes padded)
-    static constexpr int ROWS = NC * NN;             // 72 | 243 | 8 | 27
-    static constexpr int HALVES = (ROWS + 127) / 128;
-    static constexpr int CH = 32;                    // particles per chunk = 4 K-steps
-    static constexpr int KS = CH / 8;
-    static constexpr int L = 2 * ORDER + 1;
-    static constexpr int S = L * L * L;
-    static constexpr int THREADS = 128;              // one warpgroup: warp w reads TMEM lanes 32w..32w+31
-    static constexpr int TMEM_COLS = HALVES * NP <= 32 ? 32 : 64;
-    static constexpr int PARTS = X3 ? 2 : 1;         // hi (+ lo)
-    // shared memory (bytes)
-    static constexpr int A_BYTES = PARTS * KS * HALVES * 128 * 32;
-    static constexpr int B_BYTES = PARTS * KS * NP * 32;
-    static constexpr int PS_BYTES = CH * NC * 8;
-    static constexpr int PA_BYTES = CH * 9 * 8;
-    static constexpr int PW_BYTES = CH * NN * 8;
-    static constexpr int STAGE_BYTES = NN * NN * NC * 4;
-    static constexpr int OFF_A = 0;
-    static constexpr int OFF_B = OFF_A + A_BYTES;
-    static constexpr int OFF_PS = OFF_B + B_BYTES;
-    static constexpr int OFF_PA = OFF_PS + PS_BYTES;
-    static constexpr int OFF_PW = OFF_PA + PA_BYTES;
-    static constexpr int OFF_ST = OFF_PW + PW_BYTES;
-    static constexpr int OFF_ROWP = (OFF_ST + STAGE_BYTES + 15) / 16 * 16;
-    static constexpr int OFF_SLOT = OFF_ROWP + 32 * 8;
-    static constexpr int OFF_BAR = (OFF_SLOT + NN * NN * 2 + 15) / 16 * 16;
-    static constexpr int SMEM = OFF_BAR + 32;
-};
-
-// byte offset of element (row, k) (k < 8) inside one 128-row (or NP-row) K-major sub-tile
+// byte offset of element (row, k) (k < 8) inside one K-major tile of 8-row x 16-B core matrices
 __device__ __forceinline__ uint32_t kmajor_off(int row, int k)
 {
     return (uint32_t)((row >> 3) * 256 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
 }
 
+// s^{ij} = sigma q alpha^{ij} (eq_alpha_matrix) in FP32
+template <int NC>
+__device__ __forceinline__ void coeff_f(float q, float Bx, float By, float Bz, float wscale, float sigma, float s[NC])
+{
+    if (NC == 1) {
+        s[0] = sigma * q;
+    } else {
+        const float o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
+        const float d = fmaf(o0, o0, fmaf(o1, o1, fmaf(o2, o2, 1.0f)));
+        const float f = __fdiv_rn(sigma * q, d);
+        const float f0 = f * o0, f1 = f * o1, f2 = f * o2;
+        s[0] = fmaf(f0, o0, f);
+        s[1] = fmaf(f0, o1, f2);
+        s[2] = fmaf(f0, o2, -f1);
+        s[3] = fmaf(f1, o0, -f2);
+        s[4] = fmaf(f1, o1, f);
+        s[5] = fmaf(f1, o2, f0);
+        s[6] = fmaf(f2, o0, f1);
+        s[7] = fmaf(f2, o1, -f0);
+        s[8] = fmaf(f2, o2, f);
+    }
+}
+
+// Per-axis pair products of the B-spline weights.  order 1 (CIC, w = (1 - xi, xi)):
+// q = (w0 w0, w0 w1, w1 w1), index u = a + b.  order 2 (TSC, R3, R4): the
+// support base is decided in FP64 (xi >= 1/2: base 0, else -1) exactly as in the sort, then
+// u = xi - (b + 1) in [-1/2, 1/2) is rounded to FP32; w = ((1/2 - u)^2 / 2, 3/4 - u^2,
+// (1/2 + u)^2 / 2); q = (w0 w0, w0 w1, w0 w2, w1 w1, w1 w2, w2 w2), index P(a, b).
+template <int ORDER>
+__device__ __forceinline__ void pair_products(double xi, float q[ORDER == 1 ? 3 : 6])
+{
+    if (ORDER == 1) {
+        const float w1 = (float)xi, w0 = (float)(1.0 - xi);
+        q[0] = w0 * w0;
+        q[1] = w0 * w1;
+        q[2] = w1 * w1;
+    } else {
+        const float u = (float)(xi >= 0.5 ? xi - 1.0 : xi);
+        const float h = 0.5f - u, k = 0.5f + u;
+        const float w0 = (0.5f * h) * h, w1 = fmaf(-u, u, 0.75f), w2 = (0.5f * k) * k;
+        q[0] = w0 * w0;
+        q[1] = w0 * w1;
+        q[2] = w0 * w2;
+        q[3] = w1 * w1;
+        q[4] = w1 * w2;
+        q[5] = w2 * w2;
+    }
+}
+
 template <int ORDER, int NC, bool X3>
-__global__ void __launch_bounds__(128) k_asm_tf32(Geo g, const double *__restrict__ rec,
+struct PP {
+    static constexpr int NU = ORDER == 1 ? 3 : 6;      // pair products per axis
+    static constexpr int NX = NU * NU;                  // X rows: 9 | 36
+    static constexpr int NZ = NU * NC;                  // Z rows: 27 | 3 | 54 | 6
+    static constexpr int BPC = ORDER == 1 ? 4 : 2;      // bins per CTA group
+    static constexpr int MB = 128 / BPC;                // A (Z) rows per bin
+    static constexpr int NB = ORDER == 1 ? 16 : 64;     // B (X) rows per bin
+    static constexpr int N = BPC * NB;                  // MMA N: 64 | 128
+    static_assert(NZ <= MB && NX <= NB, "bin block does not fit");
+    static constexpr int CH = 32, KS = CH / 8;          // particles per chunk, K-steps
+    static constexpr int PARTS = X3 ? 2 : 1;
+    static constexpr int A_STEP = 128 * 32, B_STEP = N * 32;            // bytes per K-step
+    static constexpr int PART_BYTES = KS * (A_STEP + B_STEP);
+    static constexpr int BUF_BYTES = PARTS * PART_BYTES;
+    static constexpr int ROWS = NX + NZ;                // staging rows per bin (X then Z)
+    static constexpr int SS = 36;                       // staging row stride (floats)
+    static constexpr int L = 2 * ORDER + 1, S = L * L * L, RL = S * NC;
+    static constexpr int NDEP = 64 * NC;                // order-1 deposit entries per bin
+    static constexpr int NUNIT = 81;                    // order-2 flush units (a, b_x)
+    static constexpr int OFF_OP = 0;
+    static constexpr int OFF_STG = OFF_OP + 2 * BUF_BYTES;
+    static constexpr int OFF_EPI = OFF_STG + BPC * ROWS * SS * 4;
+    static constexpr int OFF_TAB = OFF_EPI + BPC * NX * NZ * 4;
+    static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : NUNIT * 16;
+    static constexpr int OFF_ROWP = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
+    static constexpr int OFF_BAR = OFF_ROWP + BPC * 32 * 8;
+    static constexpr int SMEM = OFF_BAR + 64;
+    static constexpr int TMEM_COLS = N;
+};
+
+template <int ORDER, int NC, bool X3>
+__global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, double wscale,
                                                   double sigma, float *__restrict__ out, float *__restrict__ ghost)
 {
-    using T = T32<ORDER, NC, X3>;
+    using T = PP<ORDER, NC, X3>;
     extern __shared__ __align__(1024) unsigned char smem[];
-    unsigned char *sA = smem + T::OFF_A;  // [PARTS][KS][HALVES][128 rows x 32 B]
-    unsigned char *sB = smem + T::OFF_B;  // [PARTS][KS][NP rows x 32 B]
-    double *ps = reinterpret_cast<double *>(smem + T::OFF_PS);  // [CH][NC]
-    double *pa = reinterpret_cast<double *>(smem + T::OFF_PA);  // [CH][9]
-    double *pw = reinterpret_cast<double *>(smem + T::OFF_PW);  // [CH][NN]
-    float *stage = reinterpret_cast<float *>(smem + T::OFF_ST); // [NN][NN][NC]
-    float **rowp = reinterpret_cast<float **>(smem + T::OFF_ROWP);
-    int16_t *s_slot = reinterpret_cast<int16_t *>(smem + T::OFF_SLOT);  // [NN][NN]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);    // [0] MMA done
-    uint32_t *s_taddr = reinterpret_cast<uint32_t *>(smem + T::OFF_BAR + 8);
+    float *stg = reinterpret_cast<float *>(smem + T::OFF_STG);   // [BPC][ROWS][SS]
+    float *epi = reinterpret_cast<float *>(smem + T::OFF_EPI);   // [BPC][NX][NZ]
+    int *tab = reinterpret_cast<int *>(smem + T::OFF_TAB);
+    float **rowp = reinterpret_cast<float **>(smem + T::OFF_ROWP);  // [BPC][32]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);  // [0..1] buffers, [2] accumulator
+    uint32_t *s_taddr = reinterpret_cast<uint32_t *>(smem + T::OFF_BAR + 32);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int plane = g.n1 * g.n2;
-    constexpr int RL = T::S * NC;
-    constexpr uint32_t IDESC = idesc_tf32(T::NP);
+    constexpr uint32_t IDESC = idesc_tf32(T::N);
 
-    for (int e = tid; e < T::NN * T::NN; e += T::THREADS) {
-        const int a = e / T::NN, b = e - T::NN * a;
-        const int ax = a / (T::N1 * T::N1), ay = (a / T::N1) % T::N1, az = a % T::N1;
-        const int bx = b / (T::N1 * T::N1), by = (b / T::N1) % T::N1, bz = b % T::N1;
-        s_slot[e] = (int16_t)(((bx - ax + ORDER) * T::L + (by - ay + ORDER)) * T::L + (bz - az + ORDER));
+    // ---- deposit tables (the FP64 kernels' address order)
+    if (ORDER == 1) {
+        // entry (a, b, c): a (3 bits) | slot*C + c (8 bits) | epilogue index x*NZ + z (11 bits)
+        for (int e = tid; e < T::NDEP; e += 128) {
+            const int a = e / (8 * NC), r = e - a * 8 * NC, b = r / NC, c = r - b * NC;
+            const int ax = a >> 2, ay = (a >> 1) & 1, az = a & 1, bx = b >> 2, by = (b >> 1) & 1, bz = b & 1;
+            const int slot = (bx - ax + 1) * 9 + (by - ay + 1) * 3 + (bz - az + 1);
+            const int x = 3 * (ax + bx) + (ay + by), z = NC * (az + bz) + c;
+            tab[e] = a | ((slot * NC + c) << 3) | ((x * T::NZ + z) << 11);
+        }
+    } else {
+        // unit (a, b_x): {a, slot(b - a)*C at b_y = b_z = 0, epilogue offsets NZ X(b_y), a_z}
+        int4 *unit = reinterpret_cast<int4 *>(tab);
+        for (int u = tid; u < T::NUNIT; u += 128) {
+            const int a = u / 3, bx = u - 3 * a;
+            const int ax = a / 9, ay = (a / 3) % 3, az = a % 3;
+            const int slot = (bx - ax + 2) * 25 + (0 - ay + 2) * 5 + (0 - az + 2);
+            const int px = ax + bx + (ax && bx);
+            int mx[3];
+            for (int by = 0; by < 3; ++by)
+                mx[by] = T::NZ * (6 * px + ay + by + (ay && by));
+            unit[u] = make_int4(a, slot * NC, mx[0] | (mx[1] << 16), mx[2] | (az << 16));
+        }
     }
-    // zero the operand buffers once: padding rows (m >= ROWS, n >= NN) stay zero
-    for (int e = tid; e < (T::A_BYTES + T::B_BYTES) / 16; e += T::THREADS)
-        reinterpret_cast<uint4 *>(smem)[e] = make_uint4(0, 0, 0, 0);
-    if (tid == 0)
+    // zero both operand buffers once: padding rows stay zero
+    for (int e = tid; e < 2 * T::BUF_BYTES / 16; e += 128)
+        reinterpret_cast<uint4 *>(smem + T::OFF_OP)[e] = make_uint4(0, 0, 0, 0);
+    if (tid == 0) {
         mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        mbar_init(&bar[2], 1);
+    }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_taddr)),
                      "n"(T::TMEM_COLS)
@@ -247,164 +286,227 @@ __global__ void __launch_bounds__(128) k_asm_tf32(Geo g, const double *__restric
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *s_taddr;
-    uint32_t mma_phase = 0;
+    const float fws = (float)wscale, fsig = (float)sigma;
 
-    for (int64_t bin = blockIdx.x; bin < nbins; bin += gridDim.x) {
-        const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
-        if (b0 == b1)
-            continue;
-        int ks_total = 0;
-        for (int base = b0; base < b1; base += T::CH) {
-            const int m = min(T::CH, b1 - base);
-            // ---- prep: one thread per particle (s in FP64, per-axis weights)
-            if (tid < m) {
-                const double *r = rec + 8 * (int64_t)(base + tid);
-                const double2 ra = *reinterpret_cast<const double2 *>(r);
-                const double2 rb = *reinterpret_cast<const double2 *>(r + 2);
-                double s[NC];
-                if (NC == 9) {
-                    const double2 rc = *reinterpret_cast<const double2 *>(r + 4);
-                    coeff<NC>(rb.y, rc.x, rc.y, r[6], wscale, sigma, s);
+    // prep role of this warp: bin pj, rows [r0, r1) of the staging (X rows then Z rows)
+    const int pj = ORDER == 1 ? warp : warp >> 1;
+    const bool do_x = ORDER == 1 || (warp & 1) == 0, do_z = ORDER == 1 || (warp & 1) == 1;
+    const int r0 = do_x ? 0 : T::NX, r1 = do_z ? T::ROWS : T::NX;
+    float *mystg = stg + pj * T::ROWS * T::SS;
+
+    uint32_t chunk_ctr = 0, group_ctr = 0;
+    const int64_t ngroups = (nbins + T::BPC - 1) / T::BPC;
+    // bin ranges of a group; the lane's record of the next chunk is loaded one chunk ahead
+    auto ranges = [&](int64_t grp, int (&bb)[T::BPC], int (&nn)[T::BPC]) {
+#pragma unroll
+        for (int j = 0; j < T::BPC; ++j) {
+            const int64_t bin = grp * T::BPC + j;
+            const bool ok = grp < ngroups && bin < nbins;
+            bb[j] = ok ? __ldg(seg_begin + bin) : 0;
+            nn[j] = ok ? __ldg(seg_begin + bin + 1) - bb[j] : 0;
+        }
+    };
+    auto load_rec = [&](int base, int n, int c, double4 &ra, double4 &rb) {
+        const int p = T::CH * c + lane;
+        if (p < n) {
+            const double *r = rec + 8 * (int64_t)(base + p);
+            ra = *reinterpret_cast<const double4 *>(r);
+            if (NC == 9)
+                rb = *reinterpret_cast<const double4 *>(r + 4);
+        }
+    };
+    int b0[T::BPC], nb[T::BPC], nb0[T::BPC], nnb[T::BPC];
+    ranges(blockIdx.x, b0, nb);
+    ranges((int64_t)blockIdx.x + gridDim.x, nb0, nnb);
+    double4 ra = make_double4(0, 0, 0, 0), rb = ra;
+    load_rec(b0[pj], nb[pj], 0, ra, rb);
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++group_ctr) {
+        int nch = 0;
+#pragma unroll
+        for (int j = 0; j < T::BPC; ++j)
+            nch = max(nch, (nb[j] + T::CH - 1) / T::CH);
+        if (nch == 0)  // nothing was prefetched for the successor yet
+            load_rec(nb0[pj], nnb[pj], 0, ra, rb);
+        for (int c = 0; c < nch; ++c, ++chunk_ctr) {
+            const int buf = chunk_ctr & 1;
+            unsigned char *op = smem + T::OFF_OP + buf * T::BUF_BYTES;
+            const double4 ca = ra, cb = rb;
+            if (c + 1 < nch)
+                load_rec(b0[pj], nb[pj], c + 1, ra, rb);
+            else
+                load_rec(nb0[pj], nnb[pj], 0, ra, rb);
+            if (chunk_ctr >= 2)  // the MMAs that last read this buffer are done
+                mbar_wait(&bar[buf], ((chunk_ctr >> 1) - 1) & 1);
+            // ---- prep: lane = particle of the chunk; zeros past the bin's end
+            {
+                const int p = T::CH * c + lane;
+                const bool live = p < nb[pj];
+                if (live) {
+                    if (do_x) {
+                        float qx[T::NU], qy[T::NU];
+                        pair_products<ORDER>(ca.x, qx);
+                        pair_products<ORDER>(ca.y, qy);
+#pragma unroll
+                        for (int i = 0; i < T::NU; ++i)
+#pragma unroll
+                            for (int k = 0; k < T::NU; ++k)
+                                mystg[(T::NU * i + k) * T::SS + lane] = qx[i] * qy[k];
+                    }
+                    if (do_z) {
+                        float qz[T::NU], s[NC];
+                        pair_products<ORDER>(ca.z, qz);
+                        coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, s);
+#pragma unroll
+                        for (int k = 0; k < T::NU; ++k)
+#pragma unroll
+                            for (int cc = 0; cc < NC; ++cc)
+                                mystg[(T::NX + NC * k + cc) * T::SS + lane] = qz[k] * s[cc];
+                    }
                 } else {
-                    coeff<NC>(rb.y, 0, 0, 0, wscale, sigma, s);
+                    for (int rr = r0; rr < r1; ++rr)
+                        mystg[rr * T::SS + lane] = 0.0f;
                 }
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    ps[tid * NC + c] = s[c];
-                double w[3];
-                axis_weights<ORDER>(ra.x, w);
-                pa[tid * 9 + 0] = w[0]; pa[tid * 9 + 1] = w[1]; pa[tid * 9 + 2] = w[2];
-                axis_weights<ORDER>(ra.y, w);
-                pa[tid * 9 + 3] = w[0]; pa[tid * 9 + 4] = w[1]; pa[tid * 9 + 5] = w[2];
-                axis_weights<ORDER>(rb.x, w);
-                pa[tid * 9 + 6] = w[0]; pa[tid * 9 + 7] = w[1]; pa[tid * 9 + 8] = w[2];
-            } else if (tid < T::CH) {
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    ps[tid * NC + c] = 0.0;  // tail of the last K-step: s = 0 (and W = 0 below)
             }
-            __syncthreads();
-            for (int e = tid; e < T::CH * T::NN; e += T::THREADS) {
-                const int p = e / T::NN, a = e - p * T::NN;
-                double w = 0.0;
-                if (p < m) {
-                    const double *wa = pa + p * 9;
-                    w = (wa[a / (T::N1 * T::N1)] * wa[3 + (a / T::N1) % T::N1]) * wa[6 + a % T::N1];
-                }
-                pw[p * T::NN + a] = w;
-            }
-            // the previous chunk's MMAs must be done before the operand tiles are rebuilt
-            if (ks_total > 0) {
-                mbar_wait(&bar[0], mma_phase);
-                mma_phase ^= 1u;
-            }
-            __syncthreads();
-            // ---- operands: A rows m = c*NN + a, B rows n = b; TF32 (hi, lo)
-            for (int e = tid; e < T::ROWS * (T::CH / 4); e += T::THREADS) {
-                const int row = e / (T::CH / 4), k4 = e - row * (T::CH / 4);  // 4 particles per 16 B
-                const int c = row / T::NN, a = row - c * T::NN;
-                const int half = row >> 7, rr = row & 127;
+            __syncwarp();
+            // ---- staging -> TF32 K-major tiles: item = (row, 4 particles), 16-B stores
+            for (int e = lane; e < (r1 - r0) * 8; e += 32) {
+                const int rr = r0 + (e >> 3), k4 = e & 7;
+                const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * T::SS + 4 * k4);
+                const float vv[4] = {v.x, v.y, v.z, v.w};
                 uint32_t hi[4], lo[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int p = 4 * k4 + j;
-                    const float x = (float)(ps[p * NC + c] * pw[p * T::NN + a]);
-                    hi[j] = tf32_rna(x);
-                    lo[j] = tf32_rna(x - __uint_as_float(hi[j]));
+                for (int t = 0; t < 4; ++t) {
+                    hi[t] = tf32_rna(vv[t]);
+                    lo[t] = tf32_rna(vv[t] - __uint_as_float(hi[t]));
                 }
                 const int ks = k4 >> 1, kk = (k4 & 1) * 4;
-                unsigned char *dst = sA + (ks * T::HALVES + half) * 4096 + kmajor_off(rr, kk);
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+                uint32_t off;
+                if (rr < T::NX)  // B = X, rows NB j + x
+                    off = ks * (T::A_STEP + T::B_STEP) + T::A_STEP + kmajor_off(T::NB * pj + rr, kk);
+                else             // A = Z, rows MB j + z
+                    off = ks * (T::A_STEP + T::B_STEP) + kmajor_off(T::MB * pj + rr - T::NX, kk);
+                *reinterpret_cast<uint4 *>(op + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
                 if (X3)
-                    *reinterpret_cast<uint4 *>(dst + T::KS * T::HALVES * 4096) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-            }
-            for (int e = tid; e < T::NN * (T::CH / 4); e += T::THREADS) {
-                const int n = e / (T::CH / 4), k4 = e - n * (T::CH / 4);
-                uint32_t hi[4], lo[4];
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const float x = (float)pw[(4 * k4 + j) * T::NN + n];
-                    hi[j] = tf32_rna(x);
-                    lo[j] = tf32_rna(x - __uint_as_float(hi[j]));
-                }
-                const int ks = k4 >> 1, kk = (k4 & 1) * 4;
-                unsigned char *dst = sB + ks * (T::NP * 32) + kmajor_off(n, kk);
-                *reinterpret_cast<uint4 *>(dst) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                if (X3)
-                    *reinterpret_cast<uint4 *>(dst + T::KS * T::NP * 32) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+                    *reinterpret_cast<uint4 *>(op + T::PART_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
-            // ---- one thread issues the MMAs of the chunk's K-steps
             if (tid == 0) {
                 tc_fence_after();
-                const int nks = (m + 7) / 8;
-                for (int ks = 0; ks < nks; ++ks) {
+                int kmax = 0;
 #pragma unroll
-                    for (int h = 0; h < T::HALVES; ++h) {
-                        const uint32_t d = tmem + h * T::NP;
-                        const unsigned char *Ah = sA + (ks * T::HALVES + h) * 4096;
-                        const unsigned char *Bh = sB + ks * (T::NP * 32);
-                        const int acc0 = (ks_total + ks) > 0 ? 1 : 0;
-                        umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bh, 128, 256), IDESC, acc0);
-                        if (X3) {
-                            const unsigned char *Al = Ah + T::KS * T::HALVES * 4096;
-                            const unsigned char *Bl = Bh + T::KS * T::NP * 32;
-                            umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bl, 128, 256), IDESC, 1);
-                            umma_tf32(d, umma_desc(Al, 128, 256), umma_desc(Bh, 128, 256), IDESC, 1);
-                        }
+                for (int j = 0; j < T::BPC; ++j)
+                    kmax = max(kmax, min(T::CH, nb[j] - T::CH * c));
+                const int nks = (kmax + 7) / 8;
+                for (int ks = 0; ks < nks; ++ks) {
+                    const unsigned char *Ah = op + ks * (T::A_STEP + T::B_STEP);
+                    const unsigned char *Bh = Ah + T::A_STEP;
+                    const int acc0 = (c > 0 || ks > 0) ? 1 : 0;
+                    umma_tf32(tmem, umma_desc(Ah, 128, 256), umma_desc(Bh, 128, 256), IDESC, acc0);
+                    if (X3) {
+                        const unsigned char *Al = Ah + T::PART_BYTES, *Bl = Bh + T::PART_BYTES;
+                        umma_tf32(tmem, umma_desc(Ah, 128, 256), umma_desc(Bl, 128, 256), IDESC, 1);
+                        umma_tf32(tmem, umma_desc(Al, 128, 256), umma_desc(Bh, 128, 256), IDESC, 1);
                     }
                 }
-                umma_commit(&bar[0]);
+                umma_commit(&bar[buf]);
+                if (c == nch - 1)
+                    umma_commit(&bar[2]);
             }
-            ks_total += (m + 7) / 8;
-            __syncthreads();
         }
-        // ---- epilogue: wait for the accumulators, TMEM -> registers -> stage[a][b][c]
-        mbar_wait(&bar[0], mma_phase);
-        mma_phase ^= 1u;
+        // rotate the prefetched ranges (the records of the next group's first chunk are in flight)
+        int nbk[T::BPC];
+#pragma unroll
+        for (int j = 0; j < T::BPC; ++j)
+            nbk[j] = nb[j];
+#pragma unroll
+        for (int j = 0; j < T::BPC; ++j) {
+            b0[j] = nb0[j];
+            nb[j] = nnb[j];
+        }
+        ranges(grp + 2 * (int64_t)gridDim.x, nb0, nnb);
+        if (nch == 0)
+            continue;
+        // ---- epilogue: accumulators -> epi[j][x][z]
+        const int bins_here = (int)min((int64_t)T::BPC, nbins - grp * T::BPC);
+        if (ORDER == 1) {
+            if (lane < 8 && warp < bins_here) {
+                const int64_t bin = grp * T::BPC + warp;
+                const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+                const int by = rem / g.n2, bz = rem - by * g.n2;
+                rowp[warp * 32 + lane] = row_ptr_f(g, g.x_begin + bx + (lane >> 2), wrapi(by + ((lane >> 1) & 1), g.n1),
+                                                   wrapi(bz + (lane & 1), g.n2), out, ghost, T::RL);
+            }
+        } else {
+            if ((warp & 1) == 0 && lane < 27 && (warp >> 1) < bins_here) {
+                const int64_t bin = grp * T::BPC + (warp >> 1);
+                const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+                const int by = rem / g.n2, bz = rem - by * g.n2;
+                const int a = lane;
+                rowp[(warp >> 1) * 32 + a] = row_ptr_f(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
+                                                       wrapi(bz + a % 3, g.n2), out, ghost, T::RL);
+            }
+        }
+        mbar_wait(&bar[2], group_ctr & 1);
         tc_fence_after();
-        const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
-        const int by = rem / g.n2, bz = rem - by * g.n2;
-        if (tid < T::NN) {
-            const int a = tid;
-            const int ax = a / (T::N1 * T::N1), ay = (a / T::N1) % T::N1, az = a % T::N1;
-            rowp[a] = row_ptr_f(g, g.x_begin + bx - (ORDER - 1) + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2), out,
-                                ghost, RL);
-        }
         {
-            const int quarter = warp & 3;      // TMEM lanes 32*quarter .. +31
-            constexpr int NCG = T::THREADS / 128;  // column groups (warps sharing a lane quarter)
-            const int cgrp = warp >> 2;
+            const int j = ORDER == 1 ? warp : warp >> 1;
+            const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
+            float *ep = epi + j * T::NX * T::NZ;
+            const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * j;
 #pragma unroll
-            for (int h = 0; h < T::HALVES; ++h) {
-                const int row = h * 128 + quarter * 32 + lane;
-                for (int c0 = cgrp * 8; c0 < T::NP; c0 += 8 * NCG) {
-                    float v[8];
-                    tmem_ld8(tmem + ((uint32_t)(quarter * 32) << 16) + h * T::NP + c0, v);
-                    if (row < T::ROWS) {
-                        const int c = row / T::NN, a = row - c * T::NN;
+            for (int x0 = 0; x0 < T::NX; x0 += 16) {
+                float v[16];
+                tmem_ld16(tl + x0, v);
+                tmem_wait_ld();
+                if (z < T::NZ) {
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) {
-                            const int b = c0 + j;
-                            if (b < T::NN)
-                                stage[(a * T::NN + b) * NC + c] = v[j];
-                        }
-                    }
+                    for (int i = 0; i < 16; ++i)
+                        if (x0 + i < T::NX)
+                            ep[(x0 + i) * T::NZ + z] = v[i];
                 }
             }
         }
         tc_fence_before();
         __syncthreads();
-        // ---- flush in address order: e = (a*NN + b)*NC + c -> row(a) + slot(a,b)*NC + c
-        for (int e = tid; e < T::NN * T::NN * NC; e += T::THREADS) {
-            const int ab = NC == 1 ? e : e / NC;
-            const int c = e - ab * NC;
-            const float v = stage[e];
-            if (v != 0.0f)
-                red_add_f32(rowp[ab / T::NN] + s_slot[ab] * NC + c, v);
+        // ---- deposit: FP32 REDs in global address order
+        if (ORDER == 1) {
+            if (warp < bins_here && nbk[warp] > 0) {
+                const float *ep = epi + warp * T::NX * T::NZ;
+                float *myrow = rowp[warp * 32 + (lane & 7)];
+                for (int i = 0; i < T::NDEP; i += 32) {
+                    const bool ok = i + lane < T::NDEP;
+                    const int t = ok ? tab[i + lane] : 0;
+                    unsigned long long rp = (unsigned long long)myrow;
+                    const unsigned lo32 = __shfl_sync(0xffffffffu, (unsigned)rp, t & 7);
+                    const unsigned hi32 = __shfl_sync(0xffffffffu, (unsigned)(rp >> 32), t & 7);
+                    float *row = (float *)(((unsigned long long)hi32 << 32) | lo32);
+                    if (ok)
+                        red_add_f32(row + ((t >> 3) & 255), ep[t >> 11]);
+                }
+            }
+        } else {
+            const int j = warp >> 1;
+            const int RUN = 3 * NC;
+            if (j < bins_here && nbk[j] > 0 && lane < RUN) {
+                const float *ep = epi + j * T::NX * T::NZ;
+                const int4 *unit = reinterpret_cast<const int4 *>(tab);
+                const int lbz = lane / NC, lc = lane - NC * lbz;
+                const int noff0 = NC * lbz + lc;                        // P(0, bz) = bz
+                const int noff1 = NC * (lbz + 1 + (lbz > 0)) + lc;      // P(1, bz) = 1, 3, 4
+                const int noff2 = NC * (lbz == 0 ? 2 : lbz + 3) + lc;   // P(2, bz) = 2, 4, 5
+                for (int u = warp & 1; u < T::NUNIT; u += 2) {
+                    const int4 t = unit[u];
+                    const int az = t.w >> 16;
+                    const int no = az == 0 ? noff0 : (az == 1 ? noff1 : noff2);
+                    float *p = rowp[j * 32 + t.x] + t.y + lane;
+                    red_add_f32(p, ep[(t.z & 0xffff) + no]);
+                    red_add_f32(p + 5 * NC, ep[(t.z >> 16) + no]);
+                    red_add_f32(p + 10 * NC, ep[(t.w & 0xffff) + no]);
+                }
+            }
         }
-        __syncthreads();
+        // the next group's epilogue rewrites epi / rowp only after its chunk barriers
     }
     tc_fence_before();
     __syncthreads();
@@ -415,7 +517,7 @@ __global__ void __launch_bounds__(128) k_asm_tf32(Geo g, const double *__restric
 template <int ORDER, int NC, bool X3>
 cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
 {
-    using T = T32<ORDER, NC, X3>;
+    using T = PP<ORDER, NC, X3>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_asm_tf32<ORDER, NC, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -424,27 +526,25 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
             return e;
         attr = true;
     }
-    int per_sm = 0, dev = 0, sms = 148, smem_sm = 0;
+    int dev = 0, sms = 148, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // resident CTAs per SM from smem / threads / registers (the occupancy API reports 1 for
-    // this kernel), then capped by TMEM columns below
     cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k_asm_tf32<ORDER, NC, X3>);
-    per_sm = smem_sm / (T::SMEM + 1024);
-    per_sm = min(per_sm, 2048 / T::THREADS);
+    // resident CTAs per SM from smem / threads / registers, capped by the 512 TMEM columns
+    int per_sm = smem_sm / (T::SMEM + 1024);
+    per_sm = min(per_sm, 2048 / 128);
     if (fa.numRegs > 0)
-        per_sm = min(per_sm, 65536 / (fa.numRegs * T::THREADS));
-    per_sm = min(per_sm, 16);
+        per_sm = min(per_sm, 65536 / (fa.numRegs * 128));
+    per_sm = min(per_sm, 512 / T::TMEM_COLS);
     if (per_sm < 1)
         per_sm = 1;
-    if (per_sm * T::TMEM_COLS > 512)
-        per_sm = 512 / T::TMEM_COLS;
+    const int64_t ngroups = (a.nbins + T::BPC - 1) / T::BPC;
     int64_t grid = (int64_t)sms * per_sm;
-    if (grid > a.nbins)
-        grid = a.nbins;
-    k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, T::THREADS, T::SMEM, s>>>(
+    if (grid > ngroups)
+        grid = ngroups;
+    k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, 128, T::SMEM, s>>>(
         geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, reinterpret_cast<float *>(a.out),
         reinterpret_cast<float *>(a.ghost));
     count_launch();
