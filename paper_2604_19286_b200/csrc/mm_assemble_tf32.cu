@@ -16,7 +16,9 @@
 // blocks cost nothing measurable, and the layout puts bin j's rows in TMEM lanes that its
 // own warp(s) can read (tcgen05.ld: warp w reads lanes 32 (w % 4) .. +31).
 //   order 1: BPC = 4, MB = 32, NB = 16, N = 64   (warp j = bin j)
-//   order 2: BPC = 2, MB = 64, NB = 64, N = 128  (warps 2j, 2j+1 = bin j: X / Z prep, lane halves)
+//   order 2: BPC = 2, MB = 64, NB = 64, N = 128
+// 8 warps per CTA: each bin has 2 (order 1) or 4 (order 2) warps that split its X / Z rows in
+// the prep and its entries in the deposit; warps 0-3 read the accumulators (lane quarter = warp).
 // Per 32-particle chunk: prep (FP32 from the FP64 record; the support base is decided in FP64
 // exactly as in the sort) -> staging [row][particle] -> TF32 (cvt.rna) K-major tiles (no-swizzle
 // canonical layout: 8-row x 16-B core matrices, LBO = 128 B, SBO = 256 B) in a double buffer ->
@@ -34,11 +36,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void *p)
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// Round to TF32, nearest with ties away from zero (the rounding of cvt.rna.tf32.f32, DESIGN.md
+// R16) on the bit pattern: + half an ulp of the 10-bit mantissa to the magnitude, then truncate.
+// Finite inputs only (the operands are products of weights and s).
 __device__ __forceinline__ uint32_t tf32_rna(float x)
 {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+    return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
 }
 
 __device__ __forceinline__ void red_add_f32(float *p, float v)
@@ -201,6 +204,7 @@ struct PP {
     static constexpr int NX = NU * NU;                  // X rows: 9 | 36
     static constexpr int NZ = NU * NC;                  // Z rows: 27 | 3 | 54 | 6
     static constexpr int BPC = ORDER == 1 ? 4 : 2;      // bins per CTA group
+    static constexpr int THREADS = 256, WPB = 8 / BPC;  // warps per bin
     static constexpr int MB = 128 / BPC;                // A (Z) rows per bin
     static constexpr int NB = ORDER == 1 ? 16 : 64;     // B (X) rows per bin
     static constexpr int N = BPC * NB;                  // MMA N: 64 | 128
@@ -227,7 +231,7 @@ struct PP {
 };
 
 template <int ORDER, int NC, bool X3>
-__global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(256, 2) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, double wscale,
                                                   double sigma, float *__restrict__ out, float *__restrict__ ghost)
 {
@@ -246,7 +250,7 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
     // ---- deposit tables (the FP64 kernels' address order)
     if (ORDER == 1) {
         // entry (a, b, c): a (3 bits) | slot*C + c (8 bits) | epilogue index x*NZ + z (11 bits)
-        for (int e = tid; e < T::NDEP; e += 128) {
+        for (int e = tid; e < T::NDEP; e += T::THREADS) {
             const int a = e / (8 * NC), r = e - a * 8 * NC, b = r / NC, c = r - b * NC;
             const int ax = a >> 2, ay = (a >> 1) & 1, az = a & 1, bx = b >> 2, by = (b >> 1) & 1, bz = b & 1;
             const int slot = (bx - ax + 1) * 9 + (by - ay + 1) * 3 + (bz - az + 1);
@@ -256,7 +260,7 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
     } else {
         // unit (a, b_x): {a, slot(b - a)*C at b_y = b_z = 0, epilogue offsets NZ X(b_y), a_z}
         int4 *unit = reinterpret_cast<int4 *>(tab);
-        for (int u = tid; u < T::NUNIT; u += 128) {
+        for (int u = tid; u < T::NUNIT; u += T::THREADS) {
             const int a = u / 3, bx = u - 3 * a;
             const int ax = a / 9, ay = (a / 3) % 3, az = a % 3;
             const int slot = (bx - ax + 2) * 25 + (0 - ay + 2) * 5 + (0 - az + 2);
@@ -268,7 +272,7 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
         }
     }
     // zero both operand buffers once: padding rows stay zero
-    for (int e = tid; e < 2 * T::BUF_BYTES / 16; e += 128)
+    for (int e = tid; e < 2 * T::BUF_BYTES / 16; e += T::THREADS)
         reinterpret_cast<uint4 *>(smem + T::OFF_OP)[e] = make_uint4(0, 0, 0, 0);
     if (tid == 0) {
         mbar_init(&bar[0], 1);
@@ -288,10 +292,13 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
     const uint32_t tmem = *s_taddr;
     const float fws = (float)wscale, fsig = (float)sigma;
 
-    // prep role of this warp: bin pj, rows [r0, r1) of the staging (X rows then Z rows)
-    const int pj = ORDER == 1 ? warp : warp >> 1;
-    const bool do_x = ORDER == 1 || (warp & 1) == 0, do_z = ORDER == 1 || (warp & 1) == 1;
-    const int r0 = do_x ? 0 : T::NX, r1 = do_z ? T::ROWS : T::NX;
+    // prep role of this warp: bin pj, an equal share [r0, r1) of its staging rows (X rows, then
+    // Z rows).  order 1: bin j = warps j, 4+j; order 2: bin j = warps {2j, 2j+1, 2j+4, 2j+5}, so
+    // warps 0-3 can read bin j's TMEM lane quarters (tcgen05.ld: warp w reads quarter w % 4).
+    const int pj = ORDER == 1 ? (warp & 3) : ((warp >> 1) & 1);
+    const int role = ORDER == 1 ? (warp >> 2) : ((warp & 1) + 2 * (warp >> 2));
+    const int r0 = role * T::ROWS / T::WPB, r1 = (role + 1) * T::ROWS / T::WPB;
+    const bool do_x = r0 < T::NX, do_z = r1 > T::NX;
     float *mystg = stg + pj * T::ROWS * T::SS;
 
     uint32_t chunk_ctr = 0, group_ctr = 0;
@@ -342,25 +349,22 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
                 const int p = T::CH * c + lane;
                 const bool live = p < nb[pj];
                 if (live) {
+                    float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
                     if (do_x) {
-                        float qx[T::NU], qy[T::NU];
                         pair_products<ORDER>(ca.x, qx);
                         pair_products<ORDER>(ca.y, qy);
-#pragma unroll
-                        for (int i = 0; i < T::NU; ++i)
-#pragma unroll
-                            for (int k = 0; k < T::NU; ++k)
-                                mystg[(T::NU * i + k) * T::SS + lane] = qx[i] * qy[k];
                     }
                     if (do_z) {
-                        float qz[T::NU], s[NC];
                         pair_products<ORDER>(ca.z, qz);
-                        coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, s);
+                        coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
+                    }
 #pragma unroll
-                        for (int k = 0; k < T::NU; ++k)
-#pragma unroll
-                            for (int cc = 0; cc < NC; ++cc)
-                                mystg[(T::NX + NC * k + cc) * T::SS + lane] = qz[k] * s[cc];
+                    for (int r = 0; r < T::ROWS; ++r) {
+                        if (r >= r0 && r < r1) {
+                            const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU]
+                                                      : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
+                            mystg[r * T::SS + lane] = v;
+                        }
                     }
                 } else {
                     for (int rr = r0; rr < r1; ++rr)
@@ -369,8 +373,13 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
             }
             __syncwarp();
             // ---- staging -> TF32 K-major tiles: item = (row, 4 particles), 16-B stores
-            for (int e = lane; e < (r1 - r0) * 8; e += 32) {
-                const int rr = r0 + (e >> 3), k4 = e & 7;
+            // lanes 8q..8q+7 take 8 consecutive rows at one K offset: distinct 16-B slots of the
+            // core matrices (conflict-free stores) and rows 4 banks apart in the staging (loads)
+            const int nit = ((r1 - r0 + 7) / 8) * 64;
+            for (int e = lane; e < nit; e += 32) {
+                const int rr = r0 + 8 * (e >> 6) + (e & 7), k4 = (e >> 3) & 7;
+                if (rr >= r1)
+                    continue;
                 const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * T::SS + 4 * k4);
                 const float vv[4] = {v.x, v.y, v.z, v.w};
                 uint32_t hi[4], lo[4];
@@ -427,33 +436,29 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
         ranges(grp + 2 * (int64_t)gridDim.x, nb0, nnb);
         if (nch == 0)
             continue;
-        // ---- epilogue: accumulators -> epi[j][x][z]
+        // ---- epilogue: accumulators -> epi[j][x][z] (warps 0-3 read TMEM lane quarter = warp)
         const int bins_here = (int)min((int64_t)T::BPC, nbins - grp * T::BPC);
-        if (ORDER == 1) {
-            if (lane < 8 && warp < bins_here) {
-                const int64_t bin = grp * T::BPC + warp;
-                const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
-                const int by = rem / g.n2, bz = rem - by * g.n2;
-                rowp[warp * 32 + lane] = row_ptr_f(g, g.x_begin + bx + (lane >> 2), wrapi(by + ((lane >> 1) & 1), g.n1),
-                                                   wrapi(bz + (lane & 1), g.n2), out, ghost, T::RL);
-            }
-        } else {
-            if ((warp & 1) == 0 && lane < 27 && (warp >> 1) < bins_here) {
-                const int64_t bin = grp * T::BPC + (warp >> 1);
-                const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
-                const int by = rem / g.n2, bz = rem - by * g.n2;
+        float *myrow = nullptr;  // order 1: node row of lane & 7 for bin pj
+        if (pj < bins_here) {
+            const int64_t bin = grp * T::BPC + pj;
+            const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+            const int by = rem / g.n2, bz = rem - by * g.n2;
+            if (ORDER == 1) {
+                const int a8 = lane & 7;
+                myrow = row_ptr_f(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
+                                  wrapi(bz + (a8 & 1), g.n2), out, ghost, T::RL);
+            } else if (role == 0 && lane < 27) {
                 const int a = lane;
-                rowp[(warp >> 1) * 32 + a] = row_ptr_f(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
-                                                       wrapi(bz + a % 3, g.n2), out, ghost, T::RL);
+                rowp[pj * 32 + a] = row_ptr_f(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
+                                              wrapi(bz + a % 3, g.n2), out, ghost, T::RL);
             }
         }
         mbar_wait(&bar[2], group_ctr & 1);
         tc_fence_after();
-        {
-            const int j = ORDER == 1 ? warp : warp >> 1;
+        if (warp < 4) {
             const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
-            float *ep = epi + j * T::NX * T::NZ;
-            const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * j;
+            float *ep = epi + pj * T::NX * T::NZ;
+            const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
 #pragma unroll
             for (int x0 = 0; x0 < T::NX; x0 += 16) {
                 float v[16];
@@ -469,37 +474,31 @@ __global__ void __launch_bounds__(128, 3) k_asm_tf32(Geo g, const double *__rest
         }
         tc_fence_before();
         __syncthreads();
-        // ---- deposit: FP32 REDs in global address order
-        if (ORDER == 1) {
-            if (warp < bins_here && nbk[warp] > 0) {
-                const float *ep = epi + warp * T::NX * T::NZ;
-                float *myrow = rowp[warp * 32 + (lane & 7)];
-                for (int i = 0; i < T::NDEP; i += 32) {
+        // ---- deposit: FP32 REDs in global address order, a bin's entries split over its warps
+        if (pj < bins_here && nbk[pj] > 0) {
+            const float *ep = epi + pj * T::NX * T::NZ;
+            if (ORDER == 1) {
+                for (int i = 32 * role; i < T::NDEP; i += 32 * T::WPB) {
                     const bool ok = i + lane < T::NDEP;
                     const int t = ok ? tab[i + lane] : 0;
-                    unsigned long long rp = (unsigned long long)myrow;
+                    const unsigned long long rp = (unsigned long long)myrow;
                     const unsigned lo32 = __shfl_sync(0xffffffffu, (unsigned)rp, t & 7);
                     const unsigned hi32 = __shfl_sync(0xffffffffu, (unsigned)(rp >> 32), t & 7);
                     float *row = (float *)(((unsigned long long)hi32 << 32) | lo32);
                     if (ok)
                         red_add_f32(row + ((t >> 3) & 255), ep[t >> 11]);
                 }
-            }
-        } else {
-            const int j = warp >> 1;
-            const int RUN = 3 * NC;
-            if (j < bins_here && nbk[j] > 0 && lane < RUN) {
-                const float *ep = epi + j * T::NX * T::NZ;
+            } else if (lane < 3 * NC) {
                 const int4 *unit = reinterpret_cast<const int4 *>(tab);
                 const int lbz = lane / NC, lc = lane - NC * lbz;
                 const int noff0 = NC * lbz + lc;                        // P(0, bz) = bz
                 const int noff1 = NC * (lbz + 1 + (lbz > 0)) + lc;      // P(1, bz) = 1, 3, 4
                 const int noff2 = NC * (lbz == 0 ? 2 : lbz + 3) + lc;   // P(2, bz) = 2, 4, 5
-                for (int u = warp & 1; u < T::NUNIT; u += 2) {
+                for (int u = role; u < T::NUNIT; u += T::WPB) {
                     const int4 t = unit[u];
                     const int az = t.w >> 16;
                     const int no = az == 0 ? noff0 : (az == 1 ? noff1 : noff2);
-                    float *p = rowp[j * 32 + t.x] + t.y + lane;
+                    float *p = rowp[pj * 32 + t.x] + t.y + lane;
                     red_add_f32(p, ep[(t.z & 0xffff) + no]);
                     red_add_f32(p + 5 * NC, ep[(t.z >> 16) + no]);
                     red_add_f32(p + 10 * NC, ep[(t.w & 0xffff) + no]);
@@ -534,9 +533,9 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     cudaFuncGetAttributes(&fa, k_asm_tf32<ORDER, NC, X3>);
     // resident CTAs per SM from smem / threads / registers, capped by the 512 TMEM columns
     int per_sm = smem_sm / (T::SMEM + 1024);
-    per_sm = min(per_sm, 2048 / 128);
+    per_sm = min(per_sm, 2048 / T::THREADS);
     if (fa.numRegs > 0)
-        per_sm = min(per_sm, 65536 / (fa.numRegs * 128));
+        per_sm = min(per_sm, 65536 / (fa.numRegs * T::THREADS));
     per_sm = min(per_sm, 512 / T::TMEM_COLS);
     if (per_sm < 1)
         per_sm = 1;
@@ -544,7 +543,7 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t grid = (int64_t)sms * per_sm;
     if (grid > ngroups)
         grid = ngroups;
-    k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, 128, T::SMEM, s>>>(
+    k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, T::THREADS, T::SMEM, s>>>(
         geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, reinterpret_cast<float *>(a.out),
         reinterpret_cast<float *>(a.ghost));
     count_launch();
