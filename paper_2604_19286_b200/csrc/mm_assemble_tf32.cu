@@ -231,7 +231,7 @@ struct PP {
 };
 
 template <int ORDER, int NC, bool X3>
-__global__ void __launch_bounds__(256, 2) k_asm_tf32(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, double wscale,
                                                   double sigma, float *__restrict__ out, float *__restrict__ ghost)
 {
@@ -300,6 +300,7 @@ __global__ void __launch_bounds__(256, 2) k_asm_tf32(Geo g, const double *__rest
     const int r0 = role * T::ROWS / T::WPB, r1 = (role + 1) * T::ROWS / T::WPB;
     const bool do_x = r0 < T::NX, do_z = r1 > T::NX;
     float *mystg = stg + pj * T::ROWS * T::SS;
+    const uint32_t stg_lane = smem_u32(mystg) + 4 * lane;
 
     uint32_t chunk_ctr = 0, group_ctr = 0;
     const int64_t ngroups = (nbins + T::BPC - 1) / T::BPC;
@@ -363,40 +364,50 @@ __global__ void __launch_bounds__(256, 2) k_asm_tf32(Geo g, const double *__rest
                         if (r >= r0 && r < r1) {
                             const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU]
                                                       : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-                            mystg[r * T::SS + lane] = v;
+                            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(v) : "memory");
                         }
                     }
                 } else {
                     for (int rr = r0; rr < r1; ++rr)
-                        mystg[rr * T::SS + lane] = 0.0f;
+                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + rr * T::SS * 4), "f"(0.0f) : "memory");
                 }
             }
             __syncwarp();
-            // ---- staging -> TF32 K-major tiles: item = (row, 4 particles), 16-B stores
-            // lanes 8q..8q+7 take 8 consecutive rows at one K offset: distinct 16-B slots of the
-            // core matrices (conflict-free stores) and rows 4 banks apart in the staging (loads)
-            const int nit = ((r1 - r0 + 7) / 8) * 64;
-            for (int e = lane; e < nit; e += 32) {
-                const int rr = r0 + 8 * (e >> 6) + (e & 7), k4 = (e >> 3) & 7;
-                if (rr >= r1)
-                    continue;
-                const float4 v = *reinterpret_cast<const float4 *>(mystg + rr * T::SS + 4 * k4);
-                const float vv[4] = {v.x, v.y, v.z, v.w};
-                uint32_t hi[4], lo[4];
+            // ---- staging -> TF32 K-major tiles: item = (row, 4 particles), 16-B stores.  Lanes
+            // 8q..8q+7 take 8 consecutive rows at K offset 4q (and 4q + 16): distinct 16-B slots of
+            // the core matrices (conflict-free stores), staging rows 4 banks apart (loads).
+            {
+                const uint32_t stg_s = smem_u32(mystg), op_s = smem_u32(op);
+                const int r8 = lane & 7, kq = lane >> 3;
+                for (int g8 = r0; g8 < r1; g8 += 8) {
+                    const int rr = g8 + r8;
+                    if (rr < r1) {
+                        const int trow = rr < T::NX ? T::NB * pj + rr : T::MB * pj + rr - T::NX;
+                        const uint32_t dst = op_s + (rr < T::NX ? T::A_STEP : 0) + (trow >> 3) * 256 + (trow & 7) * 16 +
+                                             (kq & 1) * 128;
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    hi[t] = tf32_rna(vv[t]);
-                    lo[t] = tf32_rna(vv[t] - __uint_as_float(hi[t]));
+                        for (int h = 0; h < 2; ++h) {
+                            float v[4];
+                            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                                         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                                         : "r"(stg_s + (uint32_t)(rr * T::SS + 4 * (kq + 4 * h)) * 4));
+                            uint32_t hi[4], lo[4];
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                hi[t] = tf32_rna(v[t]);
+                                lo[t] = tf32_rna(v[t] - __uint_as_float(hi[t]));
+                            }
+                            const uint32_t d = dst + ((kq >> 1) + 2 * h) * (T::A_STEP + T::B_STEP);
+                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d), "r"(hi[0]), "r"(hi[1]),
+                                         "r"(hi[2]), "r"(hi[3])
+                                         : "memory");
+                            if (X3)
+                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d + T::PART_BYTES),
+                                             "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
+                                             : "memory");
+                        }
+                    }
                 }
-                const int ks = k4 >> 1, kk = (k4 & 1) * 4;
-                uint32_t off;
-                if (rr < T::NX)  // B = X, rows NB j + x
-                    off = ks * (T::A_STEP + T::B_STEP) + T::A_STEP + kmajor_off(T::NB * pj + rr, kk);
-                else             // A = Z, rows MB j + z
-                    off = ks * (T::A_STEP + T::B_STEP) + kmajor_off(T::MB * pj + rr - T::NX, kk);
-                *reinterpret_cast<uint4 *>(op + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-                if (X3)
-                    *reinterpret_cast<uint4 *>(op + T::PART_BYTES + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncthreads();
