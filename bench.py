@@ -199,6 +199,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-tf32", action="store_true")
     ap.add_argument("--pipeline", action="store_true")
+    ap.add_argument("--no-c4", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -459,6 +460,84 @@ def main():
                                          (r["assemble_ms"] / 1e3) / 1e9}
                 del r
         line["tf32"] = tf
+
+    # ---- c4: 128^3 clustered (double-Harris-like) plasma, scalar (MPM-style) mass matrix, orders 1
+    #      and 2 (+ TF32 for order 2); particles drawn on the device (same recipe)
+    if world == 1 and not args.no_c4:
+        cache.clear()
+        torch.cuda.empty_cache()
+        c4 = {}
+        cfg4 = synth.config("c4o1")
+        d4 = synth.particles_device(cfg4, dev, with_B=False)
+        np4 = int(d4["q"].numel())
+        ppc4 = synth.ppc_of(cfg4)
+        sp4 = mm.Species()
+        reps = max(5, min(20, args.steps // 10))
+
+        def timed(fn, n):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record()
+            for _ in range(n):
+                fn()
+            e1.record()
+            barrier()
+            return e0.elapsed_time(e1) / n
+
+        for name, order in (("c4o1", 1), ("c4o2", 2)):
+            grid4 = mm.Grid(cfg4.n)
+            st4 = {"h": None}
+            out4 = torch.empty(mm.out_shape(grid4, order, 1), dtype=torch.float64, device=dev)
+
+            def sort4():
+                st4["h"] = mm.mm_sort_by_cell(grid4, order, 4, d4["pos"], d4["q"], None, handle=st4["h"])
+
+            def asm4(prec=mm.MM_FP64, o=out4):
+                mm.mm_assemble(st4["h"], mm.MM_SCALAR, prec, sp4, o)
+
+            for _ in range(3):
+                sort4()
+                asm4()
+            with ClockSampler(local) as clk4:
+                t_sort = timed(sort4, reps)
+                t_asm = timed(asm4, reps)
+            S = (2 * order + 1) ** 3
+            F = flops_per_particle(order, 1)
+            B = alg_bytes_per_particle(order, 1, ppc4)
+            ent = {"workload": f"{name}: 128^3, clustered double-Harris-like ppc (mean {ppc4:.2f}), "
+                               f"{'CIC' if order == 1 else 'TSC'}, scalar FP64 mass matrix",
+                   "particles": np4, "value": np4 / ((t_sort + t_asm) / 1e3) / 1e6, "unit": UNIT,
+                   "ms_per_step": t_sort + t_asm, "sort_ms": t_sort, "assemble_ms": t_asm,
+                   "assemble_mps": np4 / (t_asm / 1e3) / 1e6, "clocks": clk4.summary()}
+            hbm = np4 * B / (t_asm / 1e3) / 1e9
+            tfl = np4 * F / (t_asm / 1e3) / 1e12
+            if order == 1:  # HBM-bound (35.4 B vs 128 FLOP per particle)
+                ent["roofline"] = {"bound": "hbm", "achieved": hbm, "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                   "frac": hbm / peaks.get("hbm_gbs", 6535.1), "alg_bytes_per_particle": B,
+                                   "alg_bytes_definition": f"32 B (x, q) read + {S}x8 B output per node / ppc",
+                                   "tensor_view": {"tflops": tfl, "frac": tfl / fp64_peak}}
+            else:
+                ent["roofline"] = {"bound": "tensor", "achieved": tfl, "peak": fp64_peak, "unit": "TFLOP/s",
+                                   "frac": tfl / fp64_peak, "alg_flops_per_particle": F,
+                                   "alg_flops_definition": "F_unique = 2 x 378 node pairs x 1 comp",
+                                   "hbm_view": {"gbs": hbm, "frac": hbm / peaks.get("hbm_gbs", 6535.1)}}
+                out4f = torch.empty(mm.out_shape(grid4, order, 1), dtype=torch.float32, device=dev)
+                asm4(mm.MM_TF32, out4f)
+                t_tf = timed(lambda: asm4(mm.MM_TF32, out4f), reps)
+                Bf = 32.0 + S * 4.0 / ppc4
+                ent["tf32"] = {"assemble_ms": t_tf, "assemble_mps": np4 / (t_tf / 1e3) / 1e6,
+                               "roofline": {"bound": "hbm", "achieved": np4 * Bf / (t_tf / 1e3) / 1e9,
+                                            "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                            "frac": np4 * Bf / (t_tf / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.1),
+                                            "alg_bytes_per_particle": Bf}}
+                del out4f
+            c4[name] = ent
+            mm.mm_free(st4["h"])
+            del out4
+            torch.cuda.empty_cache()
+        line["c4"] = c4
+        del d4
+        torch.cuda.empty_cache()
 
     # ---- end to end through the public API with host buffers (pinned), H2D + D2H in the timed region
     if not args.no_e2e:

@@ -1127,6 +1127,232 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
     }
 }
 
+// ------------------------------------------------ scalar kind: pair-product GEMM, warp per bin
+// The scalar (MPM-style) mass matrix M[a][b] = sum_p sigma q_p W_a W_b with the pair-product
+// factorisation of k_asm_o1t / k_asm_o2t: X = q_x q_y (NX = 9 | 36 rows), Z = q_z sigma q
+// (NZ = 3 | 6 rows): D = X Z^T over the particles, MT = 2 | 5 row tiles x one column tile,
+// i.e. 2 | 5 DMMA per batch of 4 particles (the node-tile plan: 1 | 10).  One warp per bin
+// (static interleaved schedule), the lane's record prefetched one chunk ahead, operands staged
+// per warp ([X rows | Z rows][32 particles], zero padding rows), deposit through a table in
+// global address order (node a's row, slot(b - a)): 64 | 729 REDs per bin.
+template <int ORDER>
+struct PPS {
+    static constexpr int NU = ORDER == 1 ? 3 : 6;
+    static constexpr int NX = NU * NU, NZ = NU;
+    static constexpr int MT = (NX + 7) / 8;             // row tiles
+    static constexpr int ROWS = 8 * MT + 8;             // X rows (padded) then 8 Z rows (padded)
+    static constexpr int XS = 36;                       // row stride (doubles)
+    static constexpr int WARP_DOUBLES = ROWS * XS;
+    static constexpr int WARPS = 8;
+    static constexpr int NA = ORDER == 1 ? 8 : 27;      // support nodes
+    static constexpr int NDEP = NA * NA;                // (a, b) entries per bin
+    static constexpr int NDEP32 = (NDEP + 31) / 32 * 32;
+    static constexpr int L = 2 * ORDER + 1, S = L * L * L;
+    static constexpr size_t SMEM = (size_t)WARPS * WARP_DOUBLES * 8 + NDEP32 * 4 + WARPS * 32 * 8;
+};
+
+template <int ORDER>
+__global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const double *__restrict__ rec,
+                                                                   const int32_t *__restrict__ seg_begin,
+                                                                   int64_t nbins, double sigma,
+                                                                   double *__restrict__ out,
+                                                                   double *__restrict__ ghost)
+{
+    using L = PPS<ORDER>;
+    extern __shared__ __align__(16) double dsm_pps[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double *xz = dsm_pps + warp * L::WARP_DOUBLES;
+    int32_t *s_dep = reinterpret_cast<int32_t *>(dsm_pps + L::WARPS * L::WARP_DOUBLES);
+    double **s_rowp = reinterpret_cast<double **>(s_dep + L::NDEP32) + warp * 32;
+    const int plane = g.n1 * g.n2;
+
+    // deposit table in address order of node a's row: a (5 bits) | slot (7 bits) | stage index
+    // x * NZ + z (8 bits); padding entries have a = 31 (skipped)
+    for (int e = threadIdx.x; e < L::NDEP32; e += blockDim.x) {
+        if (e >= L::NDEP) {
+            s_dep[e] = 31;
+            continue;
+        }
+        const int a = e / L::NA, b = e - a * L::NA;
+        int ax, ay, az, bx, by, bz, x, z;
+        if (ORDER == 1) {
+            ax = a >> 2, ay = (a >> 1) & 1, az = a & 1, bx = b >> 2, by = (b >> 1) & 1, bz = b & 1;
+            x = 3 * (ax + bx) + (ay + by);
+            z = az + bz;
+        } else {
+            ax = a / 9, ay = (a / 3) % 3, az = a % 3, bx = b / 9, by = (b / 3) % 3, bz = b % 3;
+            auto P = [](int i, int j) { return i + j + (i && j); };
+            x = 6 * P(ax, bx) + P(ay, by);
+            z = P(az, bz);
+        }
+        const int slot = ((bx - ax + ORDER) * L::L + (by - ay + ORDER)) * L::L + (bz - az + ORDER);
+        s_dep[e] = a | (slot << 5) | ((x * L::NZ + z) << 12);
+    }
+    // zero padding rows (X rows NX..8MT-1, Z rows NZ..7) once
+    for (int r = 0; r < L::ROWS; ++r)
+        if ((r >= L::NX && r < 8 * L::MT) || r >= 8 * L::MT + L::NZ)
+            xz[r * L::XS + lane] = 0.0;
+    __syncthreads();
+
+    const int nw = gridDim.x * L::WARPS;
+    int bin = blockIdx.x * L::WARPS + warp;
+    int b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
+    if (bin < nbins) {
+        b0 = __ldg(seg_begin + bin);
+        b1 = __ldg(seg_begin + bin + 1);
+    }
+    if (bin + nw < nbins) {
+        nb0 = __ldg(seg_begin + bin + nw);
+        nb1 = __ldg(seg_begin + bin + nw + 1);
+    }
+    double4 ra = make_double4(0, 0, 0, 0);
+    if (bin < nbins && b0 + lane < b1)
+        ra = ld256(rec + 8 * (int64_t)(b0 + lane));
+    const int kq = lane & 3, rq = lane >> 2;
+    const double *xa = xz + rq * L::XS + kq;
+    const double *zb = xz + (8 * L::MT + rq) * L::XS + kq;
+    while (bin < nbins) {
+        int nn0 = 0, nn1 = 0;
+        if (bin + 2 * nw < nbins) {
+            nn0 = __ldg(seg_begin + bin + 2 * nw);
+            nn1 = __ldg(seg_begin + bin + 2 * nw + 1);
+        }
+        double acc[L::MT][2];
+#pragma unroll
+        for (int t = 0; t < L::MT; ++t)
+            acc[t][0] = acc[t][1] = 0.0;
+        for (int base = b0; base < b1; base += 32) {
+            const int m = min(32, b1 - base);
+            const double4 ca = ra;
+            {
+                int64_t p = -1;
+                if (base + 32 < b1) {
+                    if (base + 32 + lane < b1)
+                        p = base + 32 + lane;
+                } else if (bin + nw < nbins && nb0 + lane < nb1) {
+                    p = nb0 + lane;
+                }
+                if (p >= 0)
+                    ra = ld256(rec + 8 * p);
+            }
+            __syncwarp();
+            {
+                double qx[L::NU], qy[L::NU], qz[L::NU];
+                const bool live = lane < m;
+                if (ORDER == 1) {
+                    const double wx0 = 1.0 - ca.x, wx1 = ca.x, wy0 = 1.0 - ca.y, wy1 = ca.y, wz0 = 1.0 - ca.z,
+                                 wz1 = ca.z;
+                    qx[0] = wx0 * wx0, qx[1] = wx0 * wx1, qx[2] = wx1 * wx1;
+                    qy[0] = wy0 * wy0, qy[1] = wy0 * wy1, qy[2] = wy1 * wy1;
+                    qz[0] = wz0 * wz0, qz[1] = wz0 * wz1, qz[2] = wz1 * wz1;
+                } else {
+                    double w[3][3];
+                    weights2u(ca.x, w[0][0], w[0][1], w[0][2]);
+                    weights2u(ca.y, w[1][0], w[1][1], w[1][2]);
+                    weights2u(ca.z, w[2][0], w[2][1], w[2][2]);
+                    double *qq[3] = {qx, qy, qz};
+#pragma unroll
+                    for (int ax = 0; ax < 3; ++ax) {
+                        qq[ax][0] = w[ax][0] * w[ax][0];
+                        qq[ax][1] = w[ax][0] * w[ax][1];
+                        qq[ax][2] = w[ax][0] * w[ax][2];
+                        qq[ax][3] = w[ax][1] * w[ax][1];
+                        qq[ax][4] = w[ax][1] * w[ax][2];
+                        qq[ax][5] = w[ax][2] * w[ax][2];
+                    }
+                }
+                const double sq = live ? sigma * ca.w : 0.0;  // zero past the bin's end: exact +0
+                double *col = xz + lane;
+#pragma unroll
+                for (int i = 0; i < L::NU; ++i)
+#pragma unroll
+                    for (int j = 0; j < L::NU; ++j)
+                        col[(L::NU * i + j) * L::XS] = qx[i] * qy[j];
+#pragma unroll
+                for (int k = 0; k < L::NU; ++k)
+                    col[(8 * L::MT + k) * L::XS] = qz[k] * sq;
+            }
+            __syncwarp();
+            auto batch = [&](int kb) {
+                const double bv = zb[kb];
+#pragma unroll
+                for (int mt = 0; mt < L::MT; ++mt)
+                    dmma(acc[mt][0], acc[mt][1], xa[8 * mt * L::XS + kb], bv);
+            };
+            if (m == 32) {
+#pragma unroll
+                for (int kb = 0; kb < 32; kb += 4)
+                    batch(kb);
+            } else {
+                for (int kb = 0; kb < m; kb += 4)
+                    batch(kb);
+            }
+        }
+        if (b1 > b0) {
+            __syncwarp();
+            double *stage = xz;  // [NX][NZ] after the last batch
+#pragma unroll
+            for (int mt = 0; mt < L::MT; ++mt)
+#pragma unroll
+                for (int v = 0; v < 2; ++v) {
+                    const int x = 8 * mt + rq, z = 2 * kq + v;
+                    if (x < L::NX && z < L::NZ)
+                        stage[x * L::NZ + z] = acc[mt][v];
+                }
+            const int bx = bin / plane, rem = bin - bx * plane;
+            const int by = rem / g.n2, bz = rem - by * g.n2;
+            if (lane < L::NA) {
+                const int a = lane;
+                const int ax = ORDER == 1 ? a >> 2 : a / 9, ay = ORDER == 1 ? (a >> 1) & 1 : (a / 3) % 3,
+                          az = ORDER == 1 ? a & 1 : a % 3;
+                s_rowp[a] = row_ptr(g, g.x_begin + bx - (ORDER - 1) + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2),
+                                    out, ghost, L::S);
+            }
+            __syncwarp();
+#pragma unroll 4
+            for (int i = 0; i < L::NDEP32; i += 32) {
+                const int t = s_dep[i + lane];
+                const int a = t & 31;
+                if (a < L::NA)
+                    red_add(s_rowp[a] + ((t >> 5) & 127), stage[t >> 12]);
+            }
+            // (the stage spans X rows only, which every chunk's prep rewrites)
+        } else if (bin + nw < nbins && nb0 + lane < nb1) {
+            ra = ld256(rec + 8 * (int64_t)(nb0 + lane));
+        }
+        bin += nw;
+        b0 = nb0;
+        b1 = nb1;
+        nb0 = nn0;
+        nb1 = nn1;
+    }
+}
+
+template <int ORDER>
+cudaError_t launch_pps(const Geo &geo, const AsmArgs &a, cudaStream_t s)
+{
+    using L = PPS<ORDER>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e =
+            cudaFuncSetAttribute(k_asm_pps<ORDER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
+        if (e)
+            return e;
+        attr = true;
+    }
+    int per_sm = 0, dev = 0, sms = 148;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_asm_pps<ORDER>, L::WARPS * 32, L::SMEM);
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t want = (a.nbins + L::WARPS - 1) / L::WARPS;
+    int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
+    k_asm_pps<ORDER><<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.sigma, a.out,
+                                                          a.ghost);
+    count_launch();
+    return cudaGetLastError();
+}
+
 // Optional cap on resident assembly CTAs per SM (MM_ASM_CTAS_PER_SM): leaves room for a
 // concurrently running sort on another stream.
 inline int cta_cap()
@@ -1274,11 +1500,11 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
     if (geo.order == 1) {
         if (a.ncomp == 9)
             return legacy_tiles() ? launch_o1<9>(geo, a, s) : launch_o1t(geo, a, s);
-        return launch_o1<1>(geo, a, s);
+        return legacy_tiles() ? launch_o1<1>(geo, a, s) : launch_pps<1>(geo, a, s);
     } else {
         if (a.ncomp == 9)
             return legacy_tiles() ? launch_o2<9>(geo, a, s) : launch_o2t(geo, a, s);
-        return launch_o2<1>(geo, a, s);
+        return legacy_tiles() ? launch_o2<1>(geo, a, s) : launch_pps<2>(geo, a, s);
     }
     count_launch();
     return cudaGetLastError();

@@ -146,6 +146,42 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle=T
     return {"pos": np.ascontiguousarray(pos), "q": np.ascontiguousarray(q), "B": np.ascontiguousarray(B)}
 
 
+def particles_device(cfg: Config, device, with_B: bool = True) -> dict:
+    """The same recipe as particles() (cell counts, xi ~ U[0,1)^3, q ~ U[0.5,1.5], B ~ U[-1,1]^3,
+    uniform random input order), drawn on the GPU with torch's Philox generator seeded by
+    cfg.seed.  Same distribution, NOT the same sample as particles(): bench.py uses it for the
+    large configs (c4: 134.7 M particles) whose host generation would take minutes; no parity
+    claim rests on it."""
+    import torch
+    n0, n1, n2 = cfg.n
+    if cfg.dist == "uniform":
+        row_counts = np.full(n1, cfg.ppc, dtype=np.int64)
+    else:
+        row_counts = clustered_counts(n1, cfg.ppc)
+    gen = torch.Generator(device=device)
+    gen.manual_seed(int(cfg.seed))
+    per_plane = int(row_counts.sum()) * n2
+    total = per_plane * n0
+    cnt_yz = torch.from_numpy(np.repeat(row_counts, n2)).to(device)          # per (y, z) cell
+    yz = torch.repeat_interleave(torch.arange(n1 * n2, device=device), cnt_yz)  # [per_plane]
+    ix = torch.arange(n0, device=device).repeat_interleave(per_plane)
+    iyz = yz.repeat(n0)
+    cell = torch.stack([ix, iyz // n2, iyz % n2], dim=1).to(torch.float64)
+    del ix, iyz, yz
+    h = torch.tensor(cfg.h, dtype=torch.float64, device=device)
+    pos = (cell + torch.rand((total, 3), generator=gen, dtype=torch.float64, device=device)) * h
+    bad = torch.floor(pos / h) != cell
+    pos = torch.where(bad, cell * h, pos)
+    del cell, bad
+    q = 0.5 + torch.rand(total, generator=gen, dtype=torch.float64, device=device)
+    perm = torch.randperm(total, generator=gen, device=device)
+    out = {"pos": pos[perm].contiguous(), "q": q[perm].contiguous()}
+    del pos, q
+    if with_B:
+        out["B"] = (2.0 * torch.rand((total, 3), generator=gen, dtype=torch.float64, device=device) - 1.0)[perm]
+    return out
+
+
 def random_particles(n, np_, seed, h=(1.0, 1.0, 1.0), bscale=1.0, qrange=(0.5, 1.5)):
     """np_ particles uniformly distributed over the whole periodic box (Poisson ppc)."""
     rng = np.random.Generator(np.random.Philox(key=int(seed)))
@@ -172,5 +208,5 @@ def num_particles(cfg: Config, x_begin=0, x_end=None) -> int:
     return rows * cfg.n[2] * (x_end - x_begin)
 
 
-__all__ = ["Config", "CONFIGS", "config", "particles", "random_particles", "clustered_counts",
+__all__ = ["Config", "CONFIGS", "config", "particles", "particles_device", "random_particles", "clustered_counts",
            "num_particles", "ppc_of"]
