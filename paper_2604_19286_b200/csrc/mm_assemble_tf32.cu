@@ -223,7 +223,9 @@ struct PP {
     static constexpr int OFF_STG = OFF_OP + 2 * BUF_BYTES;
     static constexpr int OFF_EPI = OFF_STG + BPC * ROWS * SS * 4;
     static constexpr int OFF_TAB = OFF_EPI + BPC * NX * NZ * 4;
-    static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : NUNIT * 16;
+    static constexpr bool OT = ORDER == 2 && NC == 1;  // order-2 scalar: table deposit (runs of 3 are too short)
+    static constexpr int NDEP2 = 736;                   // 27 x 27 entries, padded to 32
+    static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : (OT ? NDEP2 * 4 : NUNIT * 16);
     static constexpr int OFF_ROWP = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
     static constexpr int OFF_BAR = OFF_ROWP + BPC * 32 * 8;
     static constexpr int SMEM = OFF_BAR + 64;
@@ -256,6 +258,19 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
             const int slot = (bx - ax + 1) * 9 + (by - ay + 1) * 3 + (bz - az + 1);
             const int x = 3 * (ax + bx) + (ay + by), z = NC * (az + bz) + c;
             tab[e] = a | ((slot * NC + c) << 3) | ((x * T::NZ + z) << 11);
+        }
+    } else if (T::OT) {
+        // entry (a, b): a (5 bits, 31 = padding) | slot (7 bits) | epilogue index x*NZ + z (8 bits)
+        for (int e = tid; e < T::NDEP2; e += T::THREADS) {
+            if (e >= 729) {
+                tab[e] = 31;
+                continue;
+            }
+            const int a = e / 27, b = e - 27 * a;
+            const int ax = a / 9, ay = (a / 3) % 3, az = a % 3, bx = b / 9, by = (b / 3) % 3, bz = b % 3;
+            auto P = [](int i, int j) { return i + j + (i && j); };
+            const int slot = (bx - ax + 2) * 25 + (by - ay + 2) * 5 + (bz - az + 2);
+            tab[e] = a | (slot << 5) | ((((6 * P(ax, bx) + P(ay, by)) * T::NZ) + P(az, bz)) << 12);
         }
     } else {
         // unit (a, b_x): {a, slot(b - a)*C at b_y = b_z = 0, epilogue offsets NZ X(b_y), a_z}
@@ -498,6 +513,13 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                     float *row = (float *)(((unsigned long long)hi32 << 32) | lo32);
                     if (ok)
                         red_add_f32(row + ((t >> 3) & 255), ep[t >> 11]);
+                }
+            } else if (T::OT) {
+                for (int i = 32 * role; i < T::NDEP2; i += 32 * T::WPB) {
+                    const int t = tab[i + lane];
+                    const int a = t & 31;
+                    if (a < 27)
+                        red_add_f32(rowp[pj * 32 + a] + ((t >> 5) & 127), ep[t >> 12]);
                 }
             } else if (lane < 3 * NC) {
                 const int4 *unit = reinterpret_cast<const int4 *>(tab);

@@ -1,11 +1,24 @@
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest $?
 tail -4 gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 100 --no-tf32 --no-e2e --no-cpu-baseline > gpurun_out/bench.json 2> gpurun_out/bench.err; echo bench $?
+timeout 300 python tools/time_sort.py c2 30
+MM_SORT_TIMERS=1 timeout 300 python tools/time_sort.py c2 3 2>&1 | tail -2
+timeout 300 python tools/time_sort.py c3 30
 python - <<'PY'
-import json
-d=json.loads(open('gpurun_out/bench.json').read().strip().splitlines()[-1])
-b=d['breakdown']; print('c2 step', d['ms_per_step'], 'sort', b['sort_ms'], 'asm', b['assemble_ms'], 'asm alone', b['assemble_alone_ms'])
-o=d.get('order2',{}); print('c3 step', o.get('ms_per_step'), 'sort', o.get('sort_ms'), 'asm', o.get('assemble_ms'))
+import sys, torch
+sys.path.insert(0, ".")
+import synth, paper_2604_19286_b200 as mm
+cfg = synth.config("c4o1"); d = synth.particles_device(cfg, "cuda", with_B=False)
+for order in (1, 2):
+    g = mm.Grid(cfg.n); h = None
+    for _ in range(3): h = mm.mm_sort_by_cell(g, order, 4, d["pos"], d["q"], None, handle=h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(5): h = mm.mm_sort_by_cell(g, order, 4, d["pos"], d["q"], None, handle=h)
+    e1.record(); torch.cuda.synchronize(); print("c4 sort order", order, e0.elapsed_time(e1) / 5)
+    out = torch.empty(mm.out_shape(g, order, 1), dtype=torch.float32, device="cuda")
+    for _ in range(2): mm.mm_assemble(h, 1, mm.MM_TF32, mm.Species(), out)
+    e0.record()
+    for _ in range(5): mm.mm_assemble(h, 1, mm.MM_TF32, mm.Species(), out)
+    e1.record(); torch.cuda.synchronize(); print("c4 tf32 order", order, e0.elapsed_time(e1) / 5)
+    mm.mm_free(h)
 PY
-tail -3 gpurun_out/bench.err
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-tf32 > /dev/null 2>&1; echo ncu $?
