@@ -901,7 +901,9 @@ struct O2T {
     static constexpr int ROWS = 90;                        // 36 X + 54 Z
     static constexpr int TILE = ROWS * XS;                 // one operand buffer
     static constexpr int STAGE = 36 * 54;
-    static constexpr int DOUBLES = 2 * TILE + 2 * 256 + STAGE + 28 + 2 + 162 + 4;  // xz, recs, stage, rowp, bars, units, q
+    // the stage [36][54] aliases the operand buffer of the bin's last chunk (after a barrier)
+    // one record buffer: the next chunk's TMA is issued after the barrier that ends the reads
+    static constexpr int DOUBLES = 2 * TILE + 256 + 28 + 2 + 162 + 4;  // xz, recs, rowp, bars, units, q
     static constexpr size_t SMEM = (size_t)DOUBLES * 8;
 };
 
@@ -918,7 +920,7 @@ __device__ __forceinline__ void weights2u(double xi, double &w0, double &w1, dou
     w2 = (0.5 * k) * k;
 }
 
-__global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const double *__restrict__ rec,
                                                                 const int32_t *__restrict__ seg_begin,
                                                                 int64_t nbins, double wscale, double sigma,
                                                                 double *__restrict__ out, double *__restrict__ ghost,
@@ -928,12 +930,12 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
     extern __shared__ __align__(16) double dsm_o2t[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *xzb = dsm_o2t;                                  // [2][90][XS]
-    double *srec = xzb + 2 * L::TILE;                       // [2][32 records][8]
-    double *stage = srec + 2 * 256;                         // [36][54]
-    double **rowp = reinterpret_cast<double **>(stage + L::STAGE);               // [27]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(stage + L::STAGE + 28);        // [2]
-    int4 *s_unit = reinterpret_cast<int4 *>(stage + L::STAGE + 30);             // [81]
-    int *q = reinterpret_cast<int *>(stage + L::STAGE + 30 + 162);               // cur, tnext, tnext2, issued
+    double *srec = xzb + 2 * L::TILE;                       // [32 records][8]
+    double *tail = srec + 256;
+    double **rowp = reinterpret_cast<double **>(tail);                  // [27]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(tail + 28);           // [2]
+    int4 *s_unit = reinterpret_cast<int4 *>(tail + 30);                // [81]
+    int *q = reinterpret_cast<int *>(tail + 30 + 162);                  // cur, tnext, tnext2, issued
     const int plane = g.n1 * g.n2;
     constexpr int RL = 125 * 9;
 
@@ -975,7 +977,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
         const int b0 = seg_begin[bin], b1 = seg_begin[bin + 1];
         if (threadIdx.x == 0) {
             if (b1 > b0 && q[3] != bin)
-                tma_load(srec + (chunk & 1) * 256, rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &bars[chunk & 1]);
+                tma_load(srec, rec + 8 * (int64_t)b0, min(32, b1 - b0) * 64, &bars[chunk & 1]);
             tn0 = tn1 = 0;
             if (q[1] < nbins) {
                 tn0 = seg_begin[q[1]];
@@ -991,7 +993,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
             double *xz = xzb + (chunk & 1) * L::TILE;
             mbar_wait(&bars[chunk & 1], (chunk >> 1) & 1);
             if (lane < m) {
-                const double *r = srec + (chunk & 1) * 256 + 8 * lane;
+                const double *r = srec + 8 * lane;
                 double *col = xz + lane;
                 if (warp < 2) {
                     const double2 xy = *reinterpret_cast<const double2 *>(r);
@@ -1043,7 +1045,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
                     q[3] = q[1];
                 }
                 if (cnt)
-                    tma_load(srec + ((chunk + 1) & 1) * 256, src, cnt * 64, &bars[(chunk + 1) & 1]);
+                    tma_load(srec, src, cnt * 64, &bars[(chunk + 1) & 1]);
             }
             const double *pa = xz + (8 * warp + rq) * L::XS + kq;
             const double *pb = xz + (36 + rq) * L::XS + kq;
@@ -1079,7 +1081,10 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 3) k_asm_o2t(Geo g, const dou
             bin = q[0];
             continue;
         }
-        // ---- stage[X row][Z col]
+        // ---- stage[X row][Z col] in the operand buffer of the bin's last chunk, once every
+        //      warp is done reading it
+        __syncthreads();
+        double *stage = xzb + ((chunk - 1) & 1) * L::TILE;
         {
             const int mr = 8 * warp + rq;
 #pragma unroll
