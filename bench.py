@@ -354,6 +354,28 @@ def main():
             a1.record()
             barrier()
             res["assemble_alone_ms"] = a0.elapsed_time(a1) / max(5, args.steps // 10)
+            # operator apply y = M E on the assembled matrix (NEXT-3, eq_field_eq), whole domain only
+            if not mm.is_slab(grid):
+                nrows = out.shape[0]
+                Ef = torch.rand((nrows, 3), dtype=torch.float64, device=dev, generator=None)
+                yf = torch.empty_like(Ef)
+                for _ in range(3):
+                    mm.mm_apply(grid, order, kind, out, Ef, yf)
+                p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                nap = max(10, args.steps // 5)
+                barrier()
+                p0.record()
+                for _ in range(nap):
+                    mm.mm_apply(grid, order, kind, out, Ef, yf)
+                p1.record()
+                barrier()
+                t_ap = p0.elapsed_time(p1) / nap
+                byts = nrows * (out[0].numel() * 8 + 48)
+                res["apply"] = {"ms": t_ap, "bytes_per_node": out[0].numel() * 8 + 48,
+                                "roofline": {"bound": "hbm", "achieved": byts / (t_ap / 1e3) / 1e9,
+                                             "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                             "frac": byts / (t_ap / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.1)}}
+                del Ef, yf
         res["d"] = d
         res["grid"], res["out"], res["ghost"], res["sp"], res["state"] = grid, out, ghost, sp, state
         return res
@@ -430,7 +452,8 @@ def main():
                           "sort_ms": r1.get("sort_ms"), "assemble_ms": r1["assemble_ms"],
                           "sort_nearly_sorted_input_ms": sort_nearly_ms,
                           "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
-                          "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6}}
+                          "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6},
+            "apply": r1.get("apply")}
 
     if not args.no_order2:
         r2 = measure("c3", True)
@@ -440,6 +463,7 @@ def main():
                           "c3 weak-scaled slabs", "value": r2["value"], "unit": UNIT, "ms_per_step": r2["ms_per_step"],
                           "sort_ms": r2.get("sort_ms"), "assemble_ms": r2["assemble_ms"],
                           "assemble_alone_ms": r2.get("assemble_alone_ms"), "pipelined": r2["pipelined"],
+                          "apply": r2.get("apply"),
                           "roofline": {"bound": "tensor", "kernel": "mm_assemble (k_asm_o2t + zero-fill)",
                                        "achieved": a2, "peak": fp64_peak, "unit": "TFLOP/s",
                                        "frac": a2 / fp64_peak, "alg_flops_per_particle": F2,

@@ -141,11 +141,11 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  * mm_assemble — the mass matrix of one species from a sorted handle.
  *
  * Algorithm 1: for each support-window bin (= support
- * group), batches of K_t = 4 particles build A^{ij} = W s^{ij} and B = W^T
- * (eq_AB_batch) and accumulate D^{ij} += A^{ij} B on FP64 DMMA 8x8x4 tiles
- * (eq_mma_accumulate); the finished tiles are scattered into the node-stencil
- * storage.  Order 2 pads the 27-node support to 32 and
- * computes the 10 upper 8x8 tiles (spatial symmetry, eq_spatial_symmetry).
+ * group), batches of K_t = 4 particles are contracted on FP64 DMMA 8x8x4 tiles
+ * (eq_AB_batch, eq_mma_accumulate) and the finished block is scattered into the
+ * node-stencil storage.  The operands are the per-axis pair
+ * products of the B-spline weights (W_a W_b = q_x q_y q_z, eq_shape_bspline):
+ * X = q_x q_y and Z = q_z s^{ij}, one product X Z^T per bin.
  *
  *   h          sorted handle (mm_sort_by_cell) for the same grid
  *   kind       MM_SCALAR | MM_TENSOR (MM_TENSOR needs a handle sorted with B)
@@ -168,6 +168,23 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  */
 mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp,
                       int accumulate, void *out, void *ghost, void *stream);
+
+/*
+ * mm_apply — y (+)= M E: the matrix-free product of an assembled FP64 mass
+ * matrix with a nodal field, the operation the implicit field solve performs
+ * with it ((L + sum_s M_s) E = b, eq_field_eq):
+ *   y[g][i] = sum_slot sum_j M[g][slot][3i+j] E[wrap(g + d(slot))][j]   (MM_TENSOR)
+ *   y[g]    = sum_slot M[g][slot] E[wrap(g + d(slot))]                  (MM_SCALAR)
+ *   g          host, grid; whole periodic domain only (x_begin = 0, x_end = n[0]),
+ *              else MM_ERR_INCOMPATIBLE
+ *   M          device, FP64 [n0*n1*n2][S][C] (mm_assemble's layout)
+ *   E, y       device, FP64 [n0*n1*n2][3] (MM_TENSOR) or [n0*n1*n2] (MM_SCALAR);
+ *              y must not alias E or M
+ *   accumulate 0: y = M E; 1: y += M E
+ * Asynchronous on `stream`.
+ */
+mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, const double *E, double *y,
+                   int accumulate, void *stream);
 
 /*
  * mm_ghost_add — add `nplanes` received ghost node planes into owned rows (FP64 output)

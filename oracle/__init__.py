@@ -81,6 +81,7 @@ def _load():
         lib.or_sort.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, P, P, P, P, P, P, P, P]
         lib.or_assemble.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P, P, P, P,
                                     ctypes.c_int]
+        lib.or_apply.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
         _lib = lib
     return _lib
 
@@ -203,3 +204,22 @@ def assemble(n, order, ncomp, pos, q, B=None, h=(1.0, 1.0, 1.0), qom=1.0, dt=1.0
     if rc:
         raise OracleError(rc, "assemble")
     return out
+
+
+def apply(n, order, ncomp, M, E, y=None, accumulate=False):
+    """y (+)= M E over the whole periodic grid — eq_field_eq, PAPER.md:77-83 (plain loops).
+    M: [nodes][S][ncomp]; E, y: [nodes][3] (ncomp 9) or [nodes] (ncomp 1)."""
+    g = _grid(n)
+    nn = int(n[0]) * int(n[1]) * int(n[2])
+    S = (2 * order + 1) ** 3
+    nv = 3 if ncomp == 9 else 1
+    M = _f64(M, (nn, S, ncomp))
+    E = _f64(E, (nn, nv) if nv == 3 else (nn,))
+    if y is None:
+        y = np.zeros(E.shape)
+        accumulate = False
+    assert y.dtype == np.float64 and y.flags.c_contiguous and y.size == nn * nv
+    rc = _load().or_apply(ctypes.byref(g), order, ncomp, _ptr(M), _ptr(E), _ptr(y), int(bool(accumulate)))
+    if rc:
+        raise OracleError(rc, "apply")
+    return y

@@ -354,3 +354,50 @@ int or_assemble(const or_grid *g, int order, int ncomp, const or_species *sp, in
     }
     return OR_OK;
 }
+
+/*
+ * or_apply — y (+)= M E, the product of an assembled mass matrix (node-stencil
+ * storage above) with a nodal field, as the implicit field equation uses it:
+ * (L + sum_s M_s) E = b  (eq_field_eq).  Plain definition:
+ *
+ *   y[g][i] = sum_{g'} sum_j M^{ij}_{g g'} E[g'][j]
+ *           = sum_{slot} sum_j M[g][slot][3 i + j] E[wrap(g + d(slot))][j]   (C = 9)
+ *   y[g]    = sum_{slot} M[g][slot] E[wrap(g + d(slot))]                      (C = 1)
+ *
+ * Whole periodic domain only.  E, y: [nodes][3] (C = 9) or [nodes] (C = 1).
+ */
+int or_apply(const or_grid *g, int order, int ncomp, const double *M, const double *E, double *y,
+             int accumulate)
+{
+    const int R = order, L = 2 * order + 1, S = L * L * L;
+    const int nv = ncomp == 9 ? 3 : 1;
+    int64_t gi;
+    int rc = check_grid(g, order);
+    if (rc)
+        return rc;
+    if (ncomp != 1 && ncomp != 9)
+        return OR_ERR_INVALID_ARG;
+    if (g->x_begin != 0 || g->x_end != g->n[0])
+        return OR_ERR_INVALID_ARG;
+    for (gi = 0; gi < (int64_t)g->n[0] * g->n[1] * g->n[2]; ++gi) {
+        int32_t gx = (int32_t)(gi / ((int64_t)g->n[1] * g->n[2]));
+        int32_t gy = (int32_t)((gi / g->n[2]) % g->n[1]);
+        int32_t gz = (int32_t)(gi % g->n[2]);
+        double acc[3] = {0.0, 0.0, 0.0};
+        int dx, dy, dz, i, j;
+        for (dx = -R; dx <= R; ++dx)
+            for (dy = -R; dy <= R; ++dy)
+                for (dz = -R; dz <= R; ++dz) {
+                    int slot = ((dx + R) * L + (dy + R)) * L + (dz + R);
+                    int64_t gn = ((int64_t)wrap(gx + dx, g->n[0]) * g->n[1] + wrap(gy + dy, g->n[1])) * g->n[2] +
+                                 wrap(gz + dz, g->n[2]);
+                    const double *m = M + (gi * S + slot) * ncomp;
+                    for (i = 0; i < nv; ++i)
+                        for (j = 0; j < nv; ++j)
+                            acc[i] += m[nv * i + j] * E[gn * nv + j];
+                }
+        for (i = 0; i < nv; ++i)
+            y[gi * nv + i] = accumulate ? y[gi * nv + i] + acc[i] : acc[i];
+    }
+    return OR_OK;
+}

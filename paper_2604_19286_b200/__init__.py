@@ -32,7 +32,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
                  4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sorted_view", "mm_assemble", "mm_ghost_add", "mm_ghost_planes",
+EXPORTS = ["mm_sort_by_cell", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
            "mm_out_elems", "mm_free", "mm_last_error", "mm_version", "mm_launch_count"]
 
 
@@ -80,6 +80,8 @@ def load_library(build_if_missing: bool = True):
     lib.mm_assemble.argtypes = [P, I, I, P, I, P, P, P]
     lib.mm_assemble.restype = I
     lib.mm_ghost_add.argtypes = [P, I, I, P, P, I, I, P]
+    lib.mm_apply.restype = I
+    lib.mm_apply.argtypes = [P, I, I, P, P, P, I, P]
     lib.mm_ghost_add.restype = I
     lib.mm_ghost_planes.argtypes = [I]
     lib.mm_ghost_planes.restype = I
@@ -223,6 +225,13 @@ def mm_ghost_add(grid: mm_grid, order: int, kind: int, out, recv, first_plane: i
     lib = load_library()
     _check(lib.mm_ghost_add(ctypes.byref(grid), int(order), int(kind), _dev_ptr(out, name="out"),
                             _dev_ptr(recv, name="recv"), int(first_plane), int(nplanes), _stream_ptr(stream)))
+
+
+def mm_apply(grid: mm_grid, order: int, kind: int, M, E, y, accumulate: bool = False, stream=None):
+    """y (+)= M E on the device (eq_field_eq); see include/mm.h."""
+    lib = load_library()
+    _check(lib.mm_apply(ctypes.byref(grid), int(order), int(kind), _dev_ptr(M, name="M"), _dev_ptr(E, name="E"),
+                        _dev_ptr(y, name="y"), int(bool(accumulate)), _stream_ptr(stream)))
 
 
 def mm_free(handle: Sorted):

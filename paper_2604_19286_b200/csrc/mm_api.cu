@@ -378,6 +378,29 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
     }
 }
 
+mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, const double *E, double *y,
+                   int accumulate, void *stream)
+{
+    try {
+        mm_status st = check_grid(g, order);
+        if (st)
+            return st;
+        if (kind != MM_SCALAR && kind != MM_TENSOR)
+            return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
+        if (!M || !E || !y)
+            return fail(MM_ERR_INVALID_ARG, "NULL M, E or y");
+        if (g->x_begin != 0 || g->x_end != g->n[0])
+            return fail(MM_ERR_INCOMPATIBLE, "mm_apply supports the whole periodic domain only in this version");
+        mm::Geo geo = mm::make_geo(*g, order);
+        cudaError_t e = mm::apply_enqueue(geo, (int)kind, M, E, y, accumulate ? 1 : 0, (cudaStream_t)stream);
+        if (e)
+            return cuda_fail(e, "mm_apply launch");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_apply");
+    }
+}
+
 mm_status mm_ghost_add(const mm_grid *g, int order, mm_kind kind, double *out, const double *recv, int first_plane,
                        int nplanes, void *stream)
 {

