@@ -91,11 +91,12 @@ typedef struct {
     int32_t order;     /* 1 | 2                                                   */
     int32_t k_pad;     /* K tile the bins are padded to (multiple of 4)           */
     int32_t has_B;     /* 0: scalar-only handle (sorted without B)                */
-    int32_t reserved;
+    int32_t rec_stride; /* doubles per record: 8 (sorted with B) or 4 (without B)   */
     const int32_t *perm;      /* device [np_padded]: original index, -1 = pad     */
     const int32_t *seg_begin; /* device [nbins+1]: padded exclusive scan          */
     const int32_t *seg_count; /* device [nbins]: particles per bin                */
-    const double *rec;        /* device [np_padded][8]: {xi_x,xi_y,xi_z,q,Bx,By,Bz,0} */
+    const double *rec;        /* device [np_padded][rec_stride]: {xi_x,xi_y,xi_z,q,Bx,By,Bz,0}
+                                 with B, {xi_x,xi_y,xi_z,q} for a scalar-only handle       */
 } mm_sorted_info;
 
 /*

@@ -55,7 +55,7 @@ class mm_species(ctypes.Structure):
 class mm_sorted_info(ctypes.Structure):
     _fields_ = [("np", ctypes.c_int64), ("np_padded", ctypes.c_int64), ("nbins", ctypes.c_int64),
                 ("capacity", ctypes.c_int64), ("order", ctypes.c_int32), ("k_pad", ctypes.c_int32),
-                ("has_B", ctypes.c_int32), ("reserved", ctypes.c_int32), ("perm", ctypes.c_void_p),
+                ("has_B", ctypes.c_int32), ("rec_stride", ctypes.c_int32), ("perm", ctypes.c_void_p),
                 ("seg_begin", ctypes.c_void_p), ("seg_count", ctypes.c_void_p), ("rec", ctypes.c_void_p)]
 
 
@@ -190,7 +190,7 @@ def mm_sorted_view(handle: Sorted) -> dict:
             "k_pad": info.k_pad, "has_B": bool(info.has_B),
             "perm": view(info.perm, m, "<i4"), "seg_begin": view(info.seg_begin, info.nbins + 1, "<i4"),
             "seg_count": view(info.seg_count, info.nbins, "<i4"),
-            "rec": view(info.rec, m * 8, "<f8", (m, 8))}
+            "rec": view(info.rec, m * info.rec_stride, "<f8", (m, info.rec_stride))}
 
 
 def out_shape(grid: mm_grid, order: int, kind: int):

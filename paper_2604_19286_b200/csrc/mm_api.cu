@@ -309,7 +309,7 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)
     out->order = h->order;
     out->k_pad = h->k_pad;
     out->has_B = h->has_B;
-    out->reserved = 0;
+    out->rec_stride = h->has_B ? 8 : 4;
     out->perm = h->perm;
     out->seg_begin = h->seg_begin;
     out->seg_count = h->count;
@@ -359,6 +359,7 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         mm::AsmArgs a;
         a.work = h->d_work;
         a.rec = h->rec;
+        a.rec_stride = h->has_B ? 8 : 4;
         a.seg_begin = h->seg_begin;
         a.nbins = h->nbins;
         a.ncomp = (int)kind;

@@ -1159,7 +1159,7 @@ struct PPS {
 template <int ORDER>
 __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const double *__restrict__ rec,
                                                                    const int32_t *__restrict__ seg_begin,
-                                                                   int64_t nbins, double sigma,
+                                                                   int64_t nbins, int rs, double sigma,
                                                                    double *__restrict__ out,
                                                                    double *__restrict__ ghost)
 {
@@ -1212,7 +1212,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
     }
     double4 ra = make_double4(0, 0, 0, 0);
     if (bin < nbins && b0 + lane < b1)
-        ra = ld256(rec + 8 * (int64_t)(b0 + lane));
+        ra = ld256(rec + rs * (int64_t)(b0 + lane));
     const int kq = lane & 3, rq = lane >> 2;
     const double *xa = xz + rq * L::XS + kq;
     const double *zb = xz + (8 * L::MT + rq) * L::XS + kq;
@@ -1238,7 +1238,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                     p = nb0 + lane;
                 }
                 if (p >= 0)
-                    ra = ld256(rec + 8 * p);
+                    ra = ld256(rec + rs * p);
             }
             __syncwarp();
             {
@@ -1323,7 +1323,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
             }
             // (the stage spans X rows only, which every chunk's prep rewrites)
         } else if (bin + nw < nbins && nb0 + lane < nb1) {
-            ra = ld256(rec + 8 * (int64_t)(nb0 + lane));
+            ra = ld256(rec + rs * (int64_t)(nb0 + lane));
         }
         bin += nw;
         b0 = nb0;
@@ -1352,8 +1352,8 @@ cudaError_t launch_pps(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t want = (a.nbins + L::WARPS - 1) / L::WARPS;
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
-    k_asm_pps<ORDER><<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.sigma, a.out,
-                                                          a.ghost);
+    k_asm_pps<ORDER><<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.rec_stride, a.sigma,
+                                                          a.out, a.ghost);
     count_launch();
     return cudaGetLastError();
 }
@@ -1505,11 +1505,11 @@ cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t
     if (geo.order == 1) {
         if (a.ncomp == 9)
             return legacy_tiles() ? launch_o1<9>(geo, a, s) : launch_o1t(geo, a, s);
-        return legacy_tiles() ? launch_o1<1>(geo, a, s) : launch_pps<1>(geo, a, s);
+        return launch_pps<1>(geo, a, s);  // (the node-tile kernels assume 64-B records)
     } else {
         if (a.ncomp == 9)
             return legacy_tiles() ? launch_o2<9>(geo, a, s) : launch_o2t(geo, a, s);
-        return legacy_tiles() ? launch_o2<1>(geo, a, s) : launch_pps<2>(geo, a, s);
+        return launch_pps<2>(geo, a, s);
     }
     count_launch();
     return cudaGetLastError();

@@ -234,8 +234,9 @@ struct PP {
 
 template <int ORDER, int NC, bool X3>
 __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
-                                                  const int32_t *__restrict__ seg_begin, int64_t nbins, double wscale,
-                                                  double sigma, float *__restrict__ out, float *__restrict__ ghost)
+                                                  const int32_t *__restrict__ seg_begin, int64_t nbins, int rs,
+                                                  double wscale, double sigma, float *__restrict__ out,
+                                                  float *__restrict__ ghost)
 {
     using T = PP<ORDER, NC, X3>;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -332,7 +333,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     auto load_rec = [&](int base, int n, int c, double4 &ra, double4 &rb) {
         const int p = T::CH * c + lane;
         if (p < n) {
-            const double *r = rec + 8 * (int64_t)(base + p);
+            const double *r = rec + rs * (int64_t)(base + p);
             ra = *reinterpret_cast<const double4 *>(r);
             if (NC == 9)
                 rb = *reinterpret_cast<const double4 *>(r + 4);
@@ -577,7 +578,7 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     if (grid > ngroups)
         grid = ngroups;
     k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, T::THREADS, T::SMEM, s>>>(
-        geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, reinterpret_cast<float *>(a.out),
+        geo, a.rec, a.seg_begin, a.nbins, a.rec_stride, a.wscale, a.sigma, reinterpret_cast<float *>(a.out),
         reinterpret_cast<float *>(a.ghost));
     count_launch();
     return cudaGetLastError();

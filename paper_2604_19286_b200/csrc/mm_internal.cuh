@@ -55,6 +55,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s);
 // ---- assembly (mm_assemble_fp64.cu) ----------------------------------------
 struct AsmArgs {
     const double *rec;
+    int rec_stride;       // doubles per record: 8 {xi, q, B, 0} | 4 {xi, q} (handle sorted without B)
     const int32_t *seg_begin;
     int64_t nbins;
     int ncomp;            // 1 | 9

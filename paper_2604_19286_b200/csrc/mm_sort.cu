@@ -14,7 +14,8 @@
 //   k_place    perm[seg_begin[key] + rank] = p        (order inside a bin arbitrary)
 //   k_fix_*    per bin: sort its perm slice ascending (=> STABLE), dest[perm[i]] = i,
 //              write pad slots; warp path (<= 1024), CTA path (<= 16384), huge path
-//   k_scatter  coalesced over particles: rec[dest[p]] = {xi, q, B, 0} (64-B records)
+//   k_scatter  coalesced over particles: rec[dest[p]] = {xi, q, B, 0} (64-B records;
+//              32-B {xi, q} for a scalar-only handle sorted without B)
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -292,31 +293,6 @@ __device__ __forceinline__ void st256(double *p, double a, double b, double c, d
 }
 
 
-// Record of particle p written to sorted slot i (gather mode: coalesced writes, random reads).
-struct Gather {
-    Geo g;
-    const double *pos, *q, *B;
-    double *rec;
-    int32_t *status;
-    int on;
-};
-
-__device__ __forceinline__ void gather_record(const Gather &G, int64_t i, int64_t p)
-{
-    Located L = locate(G.g, __ldg(G.pos + 3 * p), __ldg(G.pos + 3 * p + 1), __ldg(G.pos + 3 * p + 2));
-    const double qq = __ldg(G.q + p);
-    double b0 = 0.0, b1 = 0.0, b2 = 0.0;
-    if (G.B) {
-        b0 = __ldg(G.B + 3 * p);
-        b1 = __ldg(G.B + 3 * p + 1);
-        b2 = __ldg(G.B + 3 * p + 2);
-    }
-    if (!(isfinite(qq) && isfinite(b0) && isfinite(b1) && isfinite(b2)))
-        atomicOr(&G.status[ST_ERR], ERR_NONFINITE);
-    st256(G.rec + 8 * i, L.xi[0], L.xi[1], L.xi[2], qq);
-    st256(G.rec + 8 * i + 4, b0, b1, b2, 0.0);
-}
-
 // Register bitonic network over K = 32 or 64 keys (2 per lane), fully unrolled so the
 // partner distances and directions are compile-time constants.
 template <int K>
@@ -345,13 +321,15 @@ __device__ __forceinline__ void bitonic_reg(int32_t &v0, int32_t &v1, int lane)
     }
 }
 
-__device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int64_t from, int64_t to, int tid,
+// pad slots: perm -1, all-zero records (rs = record stride in doubles: 8 with B, 4 without)
+__device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int rs, int64_t from, int64_t to, int tid,
                                           int nthr)
 {
     for (int64_t i = from + tid; i < to; i += nthr) {
         perm[i] = -1;
-        st256(rec + 8 * i, 0.0, 0.0, 0.0, 0.0);
-        st256(rec + 8 * i + 4, 0.0, 0.0, 0.0, 0.0);
+        st256(rec + rs * i, 0.0, 0.0, 0.0, 0.0);
+        if (rs == 8)
+            st256(rec + rs * i + 4, 0.0, 0.0, 0.0, 0.0);
     }
 }
 
@@ -360,7 +338,7 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
                                                              int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                              double *__restrict__ rec, int32_t *__restrict__ mid_list,
                                                              int32_t *__restrict__ huge_list,
-                                                             int32_t *__restrict__ status, Gather G)
+                                                             int32_t *__restrict__ status, int rs)
 {
     __shared__ int32_t buf[FIX_WARPS][WARP_BIN_MAX];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -369,7 +347,7 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
     for (int64_t bin = (int64_t)blockIdx.x * FIX_WARPS + w; bin < nbins; bin += nwarps) {
         const int n = count[bin];
         const int64_t b = seg_begin[bin], e = seg_begin[bin + 1];
-        zero_pads(perm, rec, b + n, e, lane, 32);
+        zero_pads(perm, rec, rs, b + n, e, lane, 32);
         if (n == 0)
             continue;
         if (n > WARP_BIN_MAX) {
@@ -400,17 +378,11 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
             }
             if (lane < n) {
                 perm[b + lane] = v0;
-                if (G.on)
-                    gather_record(G, b + lane, v0);
-                else
-                    dest[v0] = (int32_t)(b + lane);
+                dest[v0] = (int32_t)(b + lane);
             }
             if (lane + 32 < n) {
                 perm[b + lane + 32] = v1;
-                if (G.on)
-                    gather_record(G, b + lane + 32, v1);
-                else
-                    dest[v1] = (int32_t)(b + lane + 32);
+                dest[v1] = (int32_t)(b + lane + 32);
             }
             continue;
         }
@@ -439,10 +411,7 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
         for (int i = lane; i < n; i += 32) {
             int32_t v = s[i];
             perm[b + i] = v;
-            if (G.on)
-                gather_record(G, b + i, v);
-            else
-                dest[v] = (int32_t)(b + i);
+            dest[v] = (int32_t)(b + i);
         }
         __syncwarp();
     }
@@ -452,7 +421,7 @@ __global__ void __launch_bounds__(1024) k_fix_cta(const int32_t *__restrict__ co
                                                   const int32_t *__restrict__ seg_begin,
                                                   int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                   const int32_t *__restrict__ mid_list,
-                                                  const int32_t *__restrict__ status, Gather G)
+                                                  const int32_t *__restrict__ status)
 {
     extern __shared__ int32_t s[];
     const int nmid = status[ST_NMID];
@@ -485,10 +454,7 @@ __global__ void __launch_bounds__(1024) k_fix_cta(const int32_t *__restrict__ co
         for (int i = threadIdx.x; i < n; i += blockDim.x) {
             int32_t v = s[i];
             perm[b + i] = v;
-            if (G.on)
-                gather_record(G, b + i, v);
-            else
-                dest[v] = (int32_t)(b + i);
+            dest[v] = (int32_t)(b + i);
         }
         __syncthreads();
     }
@@ -500,7 +466,7 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
                                                    const int32_t *__restrict__ seg_begin,
                                                    int32_t *__restrict__ perm, int32_t *__restrict__ dest,
                                                    const int32_t *__restrict__ huge_list,
-                                                   const int32_t *__restrict__ status, Gather G)
+                                                   const int32_t *__restrict__ status)
 {
     const int nhuge = status[ST_NHUGE];
     for (int it = blockIdx.x; it < nhuge; it += gridDim.x) {
@@ -513,10 +479,7 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
             int pre = block_excl_scan(f, total);
             if (f) {
                 perm[out + pre] = (int32_t)p;
-                if (G.on)
-                    gather_record(G, out + pre, p);
-                else
-                    dest[p] = (int32_t)(out + pre);
+                dest[p] = (int32_t)(out + pre);
             }
             out += total;
         }
@@ -572,9 +535,13 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const dou
         Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
         if (!(isfinite(qq[j]) && isfinite(bb[3 * j]) && isfinite(bb[3 * j + 1]) && isfinite(bb[3 * j + 2])))
             err |= ERR_NONFINITE;
-        double *r = rec + 8 * (int64_t)d[j];
-        st256(r, L.xi[0], L.xi[1], L.xi[2], qq[j]);
-        st256(r + 4, bb[3 * j], bb[3 * j + 1], bb[3 * j + 2], 0.0);
+        if (B) {
+            double *r = rec + 8 * (int64_t)d[j];
+            st256(r, L.xi[0], L.xi[1], L.xi[2], qq[j]);
+            st256(r + 4, bb[3 * j], bb[3 * j + 1], bb[3 * j + 2], 0.0);
+        } else {  // scalar-only handle: 32-B records {xi, q}
+            st256(rec + 4 * (int64_t)d[j], L.xi[0], L.xi[1], L.xi[2], qq[j]);
+        }
     }
     if (err)
         atomicOr(&status[ST_ERR], err);
@@ -643,13 +610,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         return e;
     const int T = 256;
     const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
-    // record pass: scatter (coalesced reads, random 64-B writes) or gather in the per-bin
-    // fix-up (random reads, coalesced writes); MM_SORT_GATHER=1 selects the latter
-    static const int gather_env = [] {
-        const char *v = getenv("MM_SORT_GATHER");
-        return v && v[0] == '1' ? 1 : 0;
-    }();
-    Gather G{geo, b.pos, b.q, b.B, b.rec, b.status, gather_env};
+
     if (b.np > 0) {
         if (vec)
             k_key<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
@@ -675,7 +636,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         if (grid < 1)
             grid = 1;
         k_fix_warp<<<grid, FIX_WARPS * 32, 0, s>>>(b.nbins, b.count, b.seg_begin, b.perm, b.rank, b.rec,
-                                                   b.mid_list, b.huge_list, b.status, G);
+                                                   b.mid_list, b.huge_list, b.status, b.B ? 8 : 4);
         count_launch();
         pt.mark("fix");
     }
@@ -687,14 +648,14 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
                 return e;
             attr = true;
         }
-        k_fix_cta<<<148, 1024, CTA_BIN_MAX * 4, s>>>(b.count, b.seg_begin, b.perm, b.rank, b.mid_list, b.status, G);
+        k_fix_cta<<<148, 1024, CTA_BIN_MAX * 4, s>>>(b.count, b.seg_begin, b.perm, b.rank, b.mid_list, b.status);
         count_launch();
     }
     if (b.np > CTA_BIN_MAX) {
-        k_fix_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.seg_begin, b.perm, b.rank, b.huge_list, b.status, G);
+        k_fix_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.seg_begin, b.perm, b.rank, b.huge_list, b.status);
         count_launch();
     }
-    if (b.np > 0 && !G.on) {
+    if (b.np > 0) {
         if (vec)
             k_scatter<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
                                                                       b.rec, b.status);

@@ -449,3 +449,28 @@ def test_apply_rejects_slab():
     t = torch.zeros(8, dtype=torch.float64, device="cuda")
     with pytest.raises(m.MMError):
         m.mm_apply(g, 1, 9, t, t, t)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_sort_scalar_handle_records(order):
+    # a handle sorted without B stores 32-B records {xi, q}: bit-identical to the oracle's
+    # first four record fields; assembling a B-handle as MM_SCALAR reads the 64-B records
+    n = (6, 5, 7)
+    d = synth.particles(synth.Config("t", n, order, "tensor", 13, seed=9))
+    m = mm()
+    g = m.Grid(n)
+    dd = to_dev(d)
+    h = m.mm_sort_by_cell(g, order, 4, dd["pos"], dd["q"], None)
+    v = m.mm_sorted_view(h)
+    r = oracle.sort(n, order, 4, d["pos"], d["q"], d["B"])
+    assert v["rec"].shape[1] == 4
+    assert (v["perm"].cpu().numpy() == r["perm"]).all()
+    assert (v["rec"].cpu().numpy().view(np.uint64) == r["rec"][:, :4].view(np.uint64)).all()
+    hB = m.mm_sort_by_cell(g, order, 4, dd["pos"], dd["q"], dd["B"])
+    ref = run_oracle(n, order, 1, d)
+    for hh in (h, hB):
+        for prec, dt, tol in ((m.MM_FP64, torch.float64, TOL), (m.MM_TF32, torch.float32, 2e-3)):
+            out = torch.full(m.out_shape(g, order, 1), float("nan"), dtype=dt, device="cuda")
+            m.mm_assemble(hh, 1, prec, m.Species(), out)
+            torch.cuda.synchronize()
+            assert rel_err(out.cpu().numpy().astype(np.float64), ref) <= tol
