@@ -9,7 +9,8 @@
 // DESIGN.md R13  pad slots: perm = -1, record all zeros
 //
 // Pipeline (one stream, no host sync until the very end):
-//   k_key      coalesced over particles: validate, key, rank = atomicAdd(count[key])
+//   k_key      coalesced over particles: validate, key, rank = atomicAdd(count[key]) (one
+//              atomic per run of equal keys in consecutive lanes)
 //   k_scan_*   padded exclusive scan of count -> seg_begin
 //   k_place    perm[seg_begin[key] + rank] = p        (order inside a bin arbitrary)
 //   k_fix_*    per bin: sort its perm slice ascending (=> STABLE), dest[perm[i]] = i,
@@ -108,44 +109,59 @@ __device__ __forceinline__ uint32_t bin_of(const Geo &g, const Located &L)
     return (uint32_t)(((int64_t)bx * g.n1 + by) * g.n2 + bz);
 }
 
-// Four particles per thread: more independent loads and atomics in flight.
-template <bool VEC>
-__global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const double *__restrict__ pos, uint32_t *__restrict__ key,
-                      int32_t *__restrict__ rank, int32_t *__restrict__ count, int32_t *__restrict__ status)
+// Warp-strided particles (round j: particles base + 32 j + lane, coalesced 768-B position
+// loads), 4 rounds per warp with all loads issued first.  Runs of equal keys in consecutive
+// lanes share ONE atomicAdd (the run head adds the run length; the lanes take consecutive
+// ranks): on cell-ordered input (the PIC regime) a warp's 32 particles fall into 1-3 bins, so
+// this removes the same-address atomic serialisation, and the ranks follow the particle index
+// inside each run (the per-bin fix-up then finds most slices already ascending).  On shuffled
+// input every lane is its own run (one atomic each, as before).
+__global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const double *__restrict__ pos,
+                                                uint32_t *__restrict__ key, int32_t *__restrict__ rank,
+                                                int32_t *__restrict__ count, int32_t *__restrict__ status)
 {
-    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
-    if (p0 >= np)
+    const int lane = threadIdx.x & 31;
+    const int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128;
+    if (base >= np)
         return;
-    double x[12];
-    load_vec3x4<VEC>(pos, p0, np, x);
-    uint32_t k[4];
-    int err = 0;
+    double x[4][3];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        k[j] = 0xffffffffu;
-        if (p0 + j < np) {
-            Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
+        const int64_t p = base + 32 * j + lane;
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+            x[j][m] = p < np ? __ldg(pos + 3 * p + m) : 0.0;
+    }
+    int err = 0;
+    const unsigned below = (2u << lane) - 1u;  // lanes <= lane
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t p = base + 32 * j + lane;
+        uint32_t k = 0xffffffffu;
+        if (p < np) {
+            Located L = locate(g, x[j][0], x[j][1], x[j][2]);
             if (L.err)
                 err |= L.err;
             else
-                k[j] = bin_of(g, L);
+                k = bin_of(g, L);
+        }
+        const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
+        const bool head = lane == 0 || k != kp;
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        const int h = 31 - __clz(heads & below);                 // this lane's run head
+        const unsigned after = heads & ~below;                    // heads past this lane
+        const int next = after ? __ffs(after) - 1 : 32;
+        int r = 0;
+        if (head && k != 0xffffffffu)
+            r = atomicAdd(&count[k], next - lane);               // run length (lanes lane..next-1)
+        r = __shfl_sync(0xffffffffu, r, h) + (lane - h);
+        if (p < np) {
+            key[p] = k;
+            rank[p] = r;
         }
     }
     if (err)
         atomicOr(&status[ST_ERR], err);
-    int r[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-        r[j] = (k[j] != 0xffffffffu) ? atomicAdd(&count[k[j]], 1) : 0;
-    if (p0 + 4 <= np) {
-        *reinterpret_cast<uint4 *>(key + p0) = make_uint4(k[0], k[1], k[2], k[3]);
-        *reinterpret_cast<int4 *>(rank + p0) = make_int4(r[0], r[1], r[2], r[3]);
-    } else {
-        for (int j = 0; j < 4 && p0 + j < np; ++j) {
-            key[p0 + j] = k[j];
-            rank[p0 + j] = r[j];
-        }
-    }
 }
 
 // ---- K-padded exclusive scan ----------------------------------------------
@@ -612,10 +628,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
 
     if (b.np > 0) {
-        if (vec)
-            k_key<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
-        else
-            k_key<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
+        k_key<<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
         count_launch();
         pt.mark("key");
     }
