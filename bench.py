@@ -452,6 +452,13 @@ def main():
                           "sort_ms": r1.get("sort_ms"), "assemble_ms": r1["assemble_ms"],
                           "sort_nearly_sorted_input_ms": sort_nearly_ms,
                           "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
+                          # sort against the HBM roofline: algorithmic bytes = 24 B (positions, key
+                          # pass) + 56 B (pos, q, B, record pass) read + 64 B record written
+                          "sort_roofline": {"bound": "hbm", "alg_bytes_per_particle": 144.0,
+                                            "achieved": r1["np"] * 144.0 / (r1["sort_ms"] / 1e3) / 1e9,
+                                            "unit": "GB/s", "peak": peaks.get("hbm_gbs"),
+                                            "frac": r1["np"] * 144.0 / (r1["sort_ms"] / 1e3) / 1e9 /
+                                            peaks.get("hbm_gbs", 6535.1)} if r1.get("sort_ms") else None,
                           "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6},
             "apply": r1.get("apply")}
 
