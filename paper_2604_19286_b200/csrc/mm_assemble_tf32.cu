@@ -143,11 +143,6 @@ __device__ __forceinline__ void tmem_wait_ld()
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// byte offset of element (row, k) (k < 8) inside one K-major tile of 8-row x 16-B core matrices
-__device__ __forceinline__ uint32_t kmajor_off(int row, int k)
-{
-    return (uint32_t)((row >> 3) * 256 + (k >> 2) * 128 + (row & 7) * 16 + (k & 3) * 4);
-}
 
 // s^{ij} = sigma q alpha^{ij} (eq_alpha_matrix) in FP32
 template <int NC>
@@ -228,7 +223,7 @@ struct PP {
     static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : (OT ? NDEP2 * 4 : NUNIT * 16);
     static constexpr int OFF_ROWP = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
     static constexpr int OFF_BAR = OFF_ROWP + BPC * 32 * 8;
-    static constexpr int SMEM = OFF_BAR + 64;
+    static constexpr int SMEM = OFF_BAR + 16 * 8;
     static constexpr int TMEM_COLS = N;
 };
 
@@ -244,11 +239,10 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     float *epi = reinterpret_cast<float *>(smem + T::OFF_EPI);   // [BPC][NX][NZ]
     int *tab = reinterpret_cast<int *>(smem + T::OFF_TAB);
     float **rowp = reinterpret_cast<float **>(smem + T::OFF_ROWP);  // [BPC][32]
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);  // [0..1] buffers, [2] accumulator
-    uint32_t *s_taddr = reinterpret_cast<uint32_t *>(smem + T::OFF_BAR + 32);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);  // 3 BPC mbarriers
+    uint32_t *s_taddr = reinterpret_cast<uint32_t *>(smem + T::OFF_BAR + 15 * 8);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int plane = g.n1 * g.n2;
-    constexpr uint32_t IDESC = idesc_tf32(T::N);
 
     // ---- deposit tables (the FP64 kernels' address order)
     if (ORDER == 1) {
@@ -290,11 +284,8 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     // zero both operand buffers once: padding rows stay zero
     for (int e = tid; e < 2 * T::BUF_BYTES / 16; e += T::THREADS)
         reinterpret_cast<uint4 *>(smem + T::OFF_OP)[e] = make_uint4(0, 0, 0, 0);
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        mbar_init(&bar[2], 1);
-    }
+    if (tid < 3 * T::BPC)
+        mbar_init(&bar[tid], 1);  // [2 pj + buf] operand buffers, [2 BPC + pj] accumulators
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(s_taddr)),
                      "n"(T::TMEM_COLS)
@@ -318,17 +309,22 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     float *mystg = stg + pj * T::ROWS * T::SS;
     const uint32_t stg_lane = smem_u32(mystg) + 4 * lane;
 
-    uint32_t chunk_ctr = 0, group_ctr = 0;
+    // Each bin slot pj (its 2 | 4 warps) runs independently: its own bins (group grp, slot pj),
+    // chunk double buffer parity, mbarriers, named barrier (id 1 + pj) and MMA issue into its own
+    // D columns [NB pj, NB pj + NB).  The A tile is shared: an MMA of slot pj also reads the other
+    // slots' rows (possibly while they are rewritten), which only produce D lanes outside its
+    // quarter(s), never read.
+    const int pthreads = 32 * T::WPB;
+    const bool issuer = role == 0 && lane == 0;
+    uint64_t *bar_buf = bar + 2 * pj, *bar_acc = bar + 2 * T::BPC + pj;
+    constexpr uint32_t IDESC_J = idesc_tf32(T::NB);
+    uint32_t cc = 0, bc = 0;  // chunks / non-empty bins of this slot
     const int64_t ngroups = (nbins + T::BPC - 1) / T::BPC;
-    // bin ranges of a group; the lane's record of the next chunk is loaded one chunk ahead
-    auto ranges = [&](int64_t grp, int (&bb)[T::BPC], int (&nn)[T::BPC]) {
-#pragma unroll
-        for (int j = 0; j < T::BPC; ++j) {
-            const int64_t bin = grp * T::BPC + j;
-            const bool ok = grp < ngroups && bin < nbins;
-            bb[j] = ok ? __ldg(seg_begin + bin) : 0;
-            nn[j] = ok ? __ldg(seg_begin + bin + 1) - bb[j] : 0;
-        }
+    auto range = [&](int64_t grp, int &bb, int &nn) {
+        const int64_t bin = grp * T::BPC + pj;
+        const bool ok = grp < ngroups && bin < nbins;
+        bb = ok ? __ldg(seg_begin + bin) : 0;
+        nn = ok ? __ldg(seg_begin + bin + 1) - bb : 0;
     };
     auto load_rec = [&](int base, int n, int c, double4 &ra, double4 &rb) {
         const int p = T::CH * c + lane;
@@ -339,32 +335,30 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 rb = *reinterpret_cast<const double4 *>(r + 4);
         }
     };
-    int b0[T::BPC], nb[T::BPC], nb0[T::BPC], nnb[T::BPC];
-    ranges(blockIdx.x, b0, nb);
-    ranges((int64_t)blockIdx.x + gridDim.x, nb0, nnb);
+    int b0, nb, nb0, nnb;
+    range(blockIdx.x, b0, nb);
+    range((int64_t)blockIdx.x + gridDim.x, nb0, nnb);
     double4 ra = make_double4(0, 0, 0, 0), rb = ra;
-    load_rec(b0[pj], nb[pj], 0, ra, rb);
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++group_ctr) {
-        int nch = 0;
-#pragma unroll
-        for (int j = 0; j < T::BPC; ++j)
-            nch = max(nch, (nb[j] + T::CH - 1) / T::CH);
+    load_rec(b0, nb, 0, ra, rb);
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int64_t bin = grp * T::BPC + pj;
+        const int nch = (nb + T::CH - 1) / T::CH;
         if (nch == 0)  // nothing was prefetched for the successor yet
-            load_rec(nb0[pj], nnb[pj], 0, ra, rb);
-        for (int c = 0; c < nch; ++c, ++chunk_ctr) {
-            const int buf = chunk_ctr & 1;
+            load_rec(nb0, nnb, 0, ra, rb);
+        for (int c = 0; c < nch; ++c, ++cc) {
+            const int buf = cc & 1;
             unsigned char *op = smem + T::OFF_OP + buf * T::BUF_BYTES;
             const double4 ca = ra, cb = rb;
             if (c + 1 < nch)
-                load_rec(b0[pj], nb[pj], c + 1, ra, rb);
+                load_rec(b0, nb, c + 1, ra, rb);
             else
-                load_rec(nb0[pj], nnb[pj], 0, ra, rb);
-            if (chunk_ctr >= 2)  // the MMAs that last read this buffer are done
-                mbar_wait(&bar[buf], ((chunk_ctr >> 1) - 1) & 1);
+                load_rec(nb0, nnb, 0, ra, rb);
+            if (cc >= 2)  // the MMAs of this slot that last read this buffer are done
+                mbar_wait(&bar_buf[buf], ((cc >> 1) - 1) & 1);
             // ---- prep: lane = particle of the chunk; zeros past the bin's end
             {
                 const int p = T::CH * c + lane;
-                const bool live = p < nb[pj];
+                const bool live = p < nb;
                 if (live) {
                     float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
                     if (do_x) {
@@ -426,48 +420,36 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (tid == 0) {
+            asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
+            if (issuer) {
                 tc_fence_after();
-                int kmax = 0;
-#pragma unroll
-                for (int j = 0; j < T::BPC; ++j)
-                    kmax = max(kmax, min(T::CH, nb[j] - T::CH * c));
-                const int nks = (kmax + 7) / 8;
+                const int nks = (min(T::CH, nb - T::CH * c) + 7) / 8;
                 for (int ks = 0; ks < nks; ++ks) {
                     const unsigned char *Ah = op + ks * (T::A_STEP + T::B_STEP);
-                    const unsigned char *Bh = Ah + T::A_STEP;
+                    const unsigned char *Bh = Ah + T::A_STEP + T::NB * pj * 32;
                     const int acc0 = (c > 0 || ks > 0) ? 1 : 0;
-                    umma_tf32(tmem, umma_desc(Ah, 128, 256), umma_desc(Bh, 128, 256), IDESC, acc0);
+                    const uint32_t d = tmem + T::NB * pj;
+                    umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bh, 128, 256), IDESC_J, acc0);
                     if (X3) {
                         const unsigned char *Al = Ah + T::PART_BYTES, *Bl = Bh + T::PART_BYTES;
-                        umma_tf32(tmem, umma_desc(Ah, 128, 256), umma_desc(Bl, 128, 256), IDESC, 1);
-                        umma_tf32(tmem, umma_desc(Al, 128, 256), umma_desc(Bh, 128, 256), IDESC, 1);
+                        umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bl, 128, 256), IDESC_J, 1);
+                        umma_tf32(d, umma_desc(Al, 128, 256), umma_desc(Bh, 128, 256), IDESC_J, 1);
                     }
                 }
-                umma_commit(&bar[buf]);
+                umma_commit(&bar_buf[buf]);
                 if (c == nch - 1)
-                    umma_commit(&bar[2]);
+                    umma_commit(bar_acc);
             }
         }
-        // rotate the prefetched ranges (the records of the next group's first chunk are in flight)
-        int nbk[T::BPC];
-#pragma unroll
-        for (int j = 0; j < T::BPC; ++j)
-            nbk[j] = nb[j];
-#pragma unroll
-        for (int j = 0; j < T::BPC; ++j) {
-            b0[j] = nb0[j];
-            nb[j] = nnb[j];
-        }
-        ranges(grp + 2 * (int64_t)gridDim.x, nb0, nnb);
-        if (nch == 0)
+        const int nbk = nb;
+        b0 = nb0;
+        nb = nnb;
+        range(grp + 2 * (int64_t)gridDim.x, nb0, nnb);
+        if (nch == 0 || bin >= nbins)
             continue;
-        // ---- epilogue: accumulators -> epi[j][x][z] (warps 0-3 read TMEM lane quarter = warp)
-        const int bins_here = (int)min((int64_t)T::BPC, nbins - grp * T::BPC);
-        float *myrow = nullptr;  // order 1: node row of lane & 7 for bin pj
-        if (pj < bins_here) {
-            const int64_t bin = grp * T::BPC + pj;
+        // ---- epilogue of this slot's bin: accumulators -> epi[pj][x][z]
+        float *myrow = nullptr;  // order 1: node row of lane & 7
+        {
             const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
             const int by = rem / g.n2, bz = rem - by * g.n2;
             if (ORDER == 1) {
@@ -480,9 +462,10 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                                               wrapi(bz + a % 3, g.n2), out, ghost, T::RL);
             }
         }
-        mbar_wait(&bar[2], group_ctr & 1);
+        mbar_wait(bar_acc, bc & 1);
+        ++bc;
         tc_fence_after();
-        if (warp < 4) {
+        if (warp < 4) {  // lane quarter = warp: this slot's Z rows
             const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
             float *ep = epi + pj * T::NX * T::NZ;
             const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
@@ -500,9 +483,9 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
             }
         }
         tc_fence_before();
-        __syncthreads();
-        // ---- deposit: FP32 REDs in global address order, a bin's entries split over its warps
-        if (pj < bins_here && nbk[pj] > 0) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
+        // ---- deposit: FP32 REDs in global address order, the bin's entries split over its warps
+        if (nbk > 0) {
             const float *ep = epi + pj * T::NX * T::NZ;
             if (ORDER == 1) {
                 for (int i = 32 * role; i < T::NDEP; i += 32 * T::WPB) {
@@ -539,7 +522,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 }
             }
         }
-        // the next group's epilogue rewrites epi / rowp only after its chunk barriers
+        // (epi / rowp of this slot are rewritten only after the next bin's chunk barriers)
     }
     tc_fence_before();
     __syncthreads();
