@@ -216,8 +216,8 @@ struct PP {
     static constexpr int NUNIT = 81;                    // order-2 flush units (a, b_x)
     static constexpr int OFF_OP = 0;
     static constexpr int OFF_STG = OFF_OP + 2 * BUF_BYTES;
-    static constexpr int OFF_EPI = OFF_STG + BPC * ROWS * SS * 4;
-    static constexpr int OFF_TAB = OFF_EPI + BPC * NX * NZ * 4;
+    static_assert(NX * NZ <= ROWS * SS, "the epilogue block aliases the slot's staging");
+    static constexpr int OFF_TAB = OFF_STG + BPC * ROWS * SS * 4;
     static constexpr bool OT = ORDER == 2 && NC == 1;  // order-2 scalar: table deposit (runs of 3 are too short)
     static constexpr int NDEP2 = 736;                   // 27 x 27 entries, padded to 32
     static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : (OT ? NDEP2 * 4 : NUNIT * 16);
@@ -236,7 +236,9 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     using T = PP<ORDER, NC, X3>;
     extern __shared__ __align__(1024) unsigned char smem[];
     float *stg = reinterpret_cast<float *>(smem + T::OFF_STG);   // [BPC][ROWS][SS]
-    float *epi = reinterpret_cast<float *>(smem + T::OFF_EPI);   // [BPC][NX][NZ]
+    // epi[pj] ([NX][NZ]) aliases slot pj's staging: it is written after the slot's last chunk
+    // barrier and read until the barrier that closes the deposit
+    float *epi = stg;
     int *tab = reinterpret_cast<int *>(smem + T::OFF_TAB);
     float **rowp = reinterpret_cast<float **>(smem + T::OFF_ROWP);  // [BPC][32]
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);  // 3 BPC mbarriers
@@ -467,7 +469,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
         tc_fence_after();
         if (warp < 4) {  // lane quarter = warp: this slot's Z rows
             const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
-            float *ep = epi + pj * T::NX * T::NZ;
+            float *ep = epi + pj * T::ROWS * T::SS;
             const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
 #pragma unroll
             for (int x0 = 0; x0 < T::NX; x0 += 16) {
@@ -486,7 +488,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
         asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
         // ---- deposit: FP32 REDs in global address order, the bin's entries split over its warps
         if (nbk > 0) {
-            const float *ep = epi + pj * T::NX * T::NZ;
+            const float *ep = epi + pj * T::ROWS * T::SS;
             if (ORDER == 1) {
                 for (int i = 32 * role; i < T::NDEP; i += 32 * T::WPB) {
                     const bool ok = i + lane < T::NDEP;
@@ -522,7 +524,8 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 }
             }
         }
-        // (epi / rowp of this slot are rewritten only after the next bin's chunk barriers)
+        // the slot's staging (= epi) and rowp are rewritten by the next bin
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
     }
     tc_fence_before();
     __syncthreads();
