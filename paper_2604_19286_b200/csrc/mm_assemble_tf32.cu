@@ -227,6 +227,73 @@ struct PP {
     static constexpr int TMEM_COLS = N;
 };
 
+// Prep of one warp's share [R0, R1) of a bin's staging rows (X rows, then Z rows; lane =
+// particle of the chunk, zeros past the bin's end), then the share's TF32 K-major tiles:
+// item = (row, 4 particles), 16-B stores.  Lanes 8q..8q+7 take 8 consecutive rows at K offset
+// 4q (and 4q + 16): distinct 16-B slots of the core matrices (conflict-free stores), staging
+// rows 4 banks apart (loads).  Only this warp reads its rows back: a __syncwarp suffices.
+template <int ORDER, int NC, bool X3, int ROLE>
+__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t stg_s, uint32_t op_s,
+                                          int pj, int lane, float fws, float fsig)
+{
+    using T = PP<ORDER, NC, X3>;
+    constexpr int R0 = ROLE * T::ROWS / T::WPB, R1 = (ROLE + 1) * T::ROWS / T::WPB;
+    if (ROLE >= T::WPB)
+        return;
+    const uint32_t stg_lane = stg_s + 4 * lane;
+    if (live) {
+        float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
+        if (R0 < T::NX) {
+            pair_products<ORDER>(ca.x, qx);
+            pair_products<ORDER>(ca.y, qy);
+        }
+        if (R1 > T::NX) {
+            pair_products<ORDER>(ca.z, qz);
+            coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
+        }
+#pragma unroll
+        for (int r = R0; r < R1; ++r) {
+            const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(v) : "memory");
+        }
+    } else {
+#pragma unroll
+        for (int r = R0; r < R1; ++r)
+            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(0.0f) : "memory");
+    }
+    __syncwarp();
+    const int r8 = lane & 7, kq = lane >> 3;
+#pragma unroll
+    for (int g8 = R0; g8 < R1; g8 += 8) {
+        const int rr = g8 + r8;
+        if (rr < R1) {
+            const int trow = rr < T::NX ? T::NB * pj + rr : T::MB * pj + rr - T::NX;
+            const uint32_t dst = op_s + (rr < T::NX ? T::A_STEP : 0) + (trow >> 3) * 256 + (trow & 7) * 16 + (kq & 1) * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                float v[4];
+                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                             : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
+                             : "r"(stg_s + (uint32_t)(rr * T::SS + 4 * (kq + 4 * h)) * 4));
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    hi[t] = tf32_rna(v[t]);
+                    lo[t] = tf32_rna(v[t] - __uint_as_float(hi[t]));
+                }
+                const uint32_t d = dst + ((kq >> 1) + 2 * h) * (T::A_STEP + T::B_STEP);
+                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
+                             "r"(hi[3])
+                             : "memory");
+                if (X3)
+                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d + T::PART_BYTES), "r"(lo[0]),
+                                 "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
+                                 : "memory");
+            }
+        }
+    }
+}
+
 template <int ORDER, int NC, bool X3>
 __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, int rs,
@@ -306,10 +373,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     // warps 0-3 can read bin j's TMEM lane quarters (tcgen05.ld: warp w reads quarter w % 4).
     const int pj = ORDER == 1 ? (warp & 3) : ((warp >> 1) & 1);
     const int role = ORDER == 1 ? (warp >> 2) : ((warp & 1) + 2 * (warp >> 2));
-    const int r0 = role * T::ROWS / T::WPB, r1 = (role + 1) * T::ROWS / T::WPB;
-    const bool do_x = r0 < T::NX, do_z = r1 > T::NX;
     float *mystg = stg + pj * T::ROWS * T::SS;
-    const uint32_t stg_lane = smem_u32(mystg) + 4 * lane;
 
     // Each bin slot pj (its 2 | 4 warps) runs independently: its own bins (group grp, slot pj),
     // chunk double buffer parity, mbarriers, named barrier (id 1 + pj) and MMA issue into its own
@@ -357,68 +421,15 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 load_rec(nb0, nnb, 0, ra, rb);
             if (cc >= 2)  // the MMAs of this slot that last read this buffer are done
                 mbar_wait(&bar_buf[buf], ((cc >> 1) - 1) & 1);
-            // ---- prep: lane = particle of the chunk; zeros past the bin's end
+            // ---- prep + TF32 tiles of this warp's row share (compile-time row range per role)
             {
-                const int p = T::CH * c + lane;
-                const bool live = p < nb;
-                if (live) {
-                    float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
-                    if (do_x) {
-                        pair_products<ORDER>(ca.x, qx);
-                        pair_products<ORDER>(ca.y, qy);
-                    }
-                    if (do_z) {
-                        pair_products<ORDER>(ca.z, qz);
-                        coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
-                    }
-#pragma unroll
-                    for (int r = 0; r < T::ROWS; ++r) {
-                        if (r >= r0 && r < r1) {
-                            const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU]
-                                                      : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-                            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(v) : "memory");
-                        }
-                    }
-                } else {
-                    for (int rr = r0; rr < r1; ++rr)
-                        asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + rr * T::SS * 4), "f"(0.0f) : "memory");
-                }
-            }
-            __syncwarp();
-            // ---- staging -> TF32 K-major tiles: item = (row, 4 particles), 16-B stores.  Lanes
-            // 8q..8q+7 take 8 consecutive rows at K offset 4q (and 4q + 16): distinct 16-B slots of
-            // the core matrices (conflict-free stores), staging rows 4 banks apart (loads).
-            {
-                const uint32_t stg_s = smem_u32(mystg), op_s = smem_u32(op);
-                const int r8 = lane & 7, kq = lane >> 3;
-                for (int g8 = r0; g8 < r1; g8 += 8) {
-                    const int rr = g8 + r8;
-                    if (rr < r1) {
-                        const int trow = rr < T::NX ? T::NB * pj + rr : T::MB * pj + rr - T::NX;
-                        const uint32_t dst = op_s + (rr < T::NX ? T::A_STEP : 0) + (trow >> 3) * 256 + (trow & 7) * 16 +
-                                             (kq & 1) * 128;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float v[4];
-                            asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                                         : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-                                         : "r"(stg_s + (uint32_t)(rr * T::SS + 4 * (kq + 4 * h)) * 4));
-                            uint32_t hi[4], lo[4];
-#pragma unroll
-                            for (int t = 0; t < 4; ++t) {
-                                hi[t] = tf32_rna(v[t]);
-                                lo[t] = tf32_rna(v[t] - __uint_as_float(hi[t]));
-                            }
-                            const uint32_t d = dst + ((kq >> 1) + 2 * h) * (T::A_STEP + T::B_STEP);
-                            asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d), "r"(hi[0]), "r"(hi[1]),
-                                         "r"(hi[2]), "r"(hi[3])
-                                         : "memory");
-                            if (X3)
-                                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d + T::PART_BYTES),
-                                             "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
-                                             : "memory");
-                        }
-                    }
+                const bool live = T::CH * c + lane < nb;
+                const uint32_t op_s = smem_u32(op), stg_s = smem_u32(mystg);
+                switch (role) {
+                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
+                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
+                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
+                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
