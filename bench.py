@@ -492,6 +492,47 @@ def main():
                 del r
         line["tf32"] = tf
 
+    # ---- c2 with the production storage of PAPER.md:576 (NEXT-2): FP32 positions and B, FP64
+    #      charges and mass matrix; sort + FP64 assembly per step
+    if world == 1:
+        cfg2 = synth.config("c2")
+        d2 = synth.particles(cfg2)
+        p32 = d2["pos"].astype(np.float32)
+        L32 = np.array(cfg2.n, dtype=np.float32)
+        p32 = np.where(p32 >= L32, p32 - L32, p32)  # FP32 rounding up to the box edge: periodic image
+        dm = {"pos": torch.from_numpy(p32).to(dev),
+              "q": torch.from_numpy(d2["q"]).to(dev),
+              "B": torch.from_numpy(d2["B"].astype(np.float32)).to(dev)}
+        gm = mm.Grid(cfg2.n)
+        outm = torch.empty(mm.out_shape(gm, 1, 9), dtype=torch.float64, device=dev)
+        stm = {"h": None}
+
+        def step_m():
+            stm["h"] = mm.mm_sort_by_cell(gm, 1, 4, dm["pos"], dm["q"], dm["B"], handle=stm["h"])
+            mm.mm_assemble(stm["h"], 9, mm.MM_FP64, mm.Species(), outm)
+
+        for _ in range(3):
+            step_m()
+        nm = max(10, args.steps // 10)
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        q0.record()
+        for _ in range(nm):
+            step_m()
+        q1.record()
+        barrier()
+        tm = q0.elapsed_time(q1) / nm
+        q0.record()
+        for _ in range(nm):
+            stm["h"] = mm.mm_sort_by_cell(gm, 1, 4, dm["pos"], dm["q"], dm["B"], handle=stm["h"])
+        q1.record()
+        barrier()
+        line["mixed_inputs"] = {"workload": "c2 with FP32 positions and B, FP64 q and mass matrix (PAPER.md:576)",
+                                "value": len(d2["q"]) / (tm / 1e3) / 1e6, "unit": UNIT, "ms_per_step": tm,
+                                "sort_ms": q0.elapsed_time(q1) / nm, "input_bytes_per_particle": 32}
+        mm.mm_free(stm["h"])
+        del dm, outm, d2
+
     # ---- c4: 128^3 clustered (double-Harris-like) plasma, scalar (MPM-style) mass matrix, orders 1
     #      and 2 (+ TF32 for order 2); particles drawn on the device (same recipe)
     if world == 1 and not args.no_c4:

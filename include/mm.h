@@ -135,6 +135,17 @@ typedef struct {
 mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos,
                           const double *q, const double *B, void *stream, mm_sorted **inout);
 
+/*
+ * mm_sort_by_cell_mixed — the same sort for the production storage of PAPER.md:576
+ * ("field values and particle positions are stored in FP32, while ... statistical
+ * weights and the mass matrix use FP64"): pos and B are FP32 ([np][3] each, B may be
+ * NULL), q is FP64.  Every value is widened exactly to FP64 before locate (R5), so the
+ * result equals mm_sort_by_cell on the widened arrays bit for bit; the handle's records
+ * are FP64 as always.  Arguments, ownership, errors and synchronisation as above.
+ */
+mm_status mm_sort_by_cell_mixed(const mm_grid *g, int order, int k_pad, int64_t np, const float *pos,
+                                const double *q, const float *B, void *stream, mm_sorted **inout);
+
 /* mm_sorted_view — read-only view of a handle's device arrays (see struct). */
 mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
 

@@ -32,7 +32,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
                  4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
+EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
            "mm_out_elems", "mm_free", "mm_last_error", "mm_version", "mm_launch_count"]
 
 
@@ -74,6 +74,8 @@ def load_library(build_if_missing: bool = True):
     lib = ctypes.CDLL(_build.LIB)
     P, I64, I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
     lib.mm_sort_by_cell.argtypes = [P, I, I, I64, P, P, P, P, P]
+    lib.mm_sort_by_cell_mixed.restype = I
+    lib.mm_sort_by_cell_mixed.argtypes = [P, I, I, I64, P, P, P, P, P]
     lib.mm_sort_by_cell.restype = I
     lib.mm_sorted_view.argtypes = [P, P]
     lib.mm_sorted_view.restype = I
@@ -149,18 +151,22 @@ class Sorted:
 
 def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handle: Sorted | None = None,
                     stream=None) -> Sorted:
-    """Stable support-window binning with K-padding (include/mm.h).  Reuses `handle` if given."""
+    """Stable support-window binning with K-padding (include/mm.h).  Reuses `handle` if given.
+    FP32 pos (and B) select mm_sort_by_cell_mixed (PAPER.md:576 storage; q stays FP64)."""
     lib = load_library()
+    f32 = pos is not None and pos.dtype == torch.float32
     np_ = int(pos.shape[0]) if pos is not None else 0
     if pos is not None and tuple(pos.shape) != (np_, 3):
         raise MMError(MM_ERR_INVALID_ARG, "pos must be [np, 3]")
     if B is not None and tuple(B.shape) != (np_, 3):
         raise MMError(MM_ERR_INVALID_ARG, "B must be [np, 3]")
     hp = ctypes.c_void_p(handle.ptr.value if handle is not None and handle.ptr else None)
-    st = lib.mm_sort_by_cell(ctypes.byref(grid), int(order), int(k_pad), np_,
-                             _dev_ptr(pos, name="pos") if np_ else None, _dev_ptr(q, name="q") if np_ else None,
-                             _dev_ptr(B, name="B") if (B is not None and np_) else None, _stream_ptr(stream),
-                             ctypes.byref(hp))
+    pdt = torch.float32 if f32 else torch.float64
+    fn = lib.mm_sort_by_cell_mixed if f32 else lib.mm_sort_by_cell
+    st = fn(ctypes.byref(grid), int(order), int(k_pad), np_,
+            _dev_ptr(pos, pdt, name="pos") if np_ else None, _dev_ptr(q, name="q") if np_ else None,
+            _dev_ptr(B, pdt, name="B") if (B is not None and np_) else None, _stream_ptr(stream),
+            ctypes.byref(hp))
     _check(st)
     if handle is not None:
         return handle

@@ -171,8 +171,10 @@ int64_t mm_out_elems(const mm_grid *g, int order, mm_kind kind)
     return (int64_t)(g->x_end - g->x_begin) * g->n[1] * g->n[2] * S * (int64_t)kind;
 }
 
-mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos, const double *q,
-                          const double *B, void *stream, mm_sorted **inout)
+namespace {
+// pos / B point to FP64 arrays (f32 = 0) or FP32 arrays (f32 = 1, widened exactly on load)
+mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const void *pos, const double *q,
+                      const void *B, int f32, void *stream, mm_sorted **inout)
 {
     try {
         mm_status st = check_grid(g, order);
@@ -254,9 +256,10 @@ mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, co
         b.np = np;
         b.nbins = nbins;
         b.k_pad = k_pad;
-        b.pos = pos;
+        b.pos = static_cast<const double *>(pos);
         b.q = q;
-        b.B = B;
+        b.B = static_cast<const double *>(B);
+        b.f32 = f32;
         b.key = h->key;
         b.rank = h->rank;
         b.count = h->count;
@@ -294,6 +297,20 @@ mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, co
     } catch (...) {
         return fail(MM_ERR_CUDA, "unexpected exception in mm_sort_by_cell");
     }
+}
+
+}  // namespace
+
+mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos, const double *q,
+                          const double *B, void *stream, mm_sorted **inout)
+{
+    return sort_common(g, order, k_pad, np, pos, q, B, 0, stream, inout);
+}
+
+mm_status mm_sort_by_cell_mixed(const mm_grid *g, int order, int k_pad, int64_t np, const float *pos,
+                                const double *q, const float *B, void *stream, mm_sorted **inout)
+{
+    return sort_common(g, order, k_pad, np, pos, q, B, 1, stream, inout);
 }
 
 mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)

@@ -37,6 +37,7 @@ struct SortBufs {
     int64_t np, nbins;
     int k_pad;
     const double *pos, *q, *B;
+    int f32;             // 1: pos and B point to FP32 arrays (widened exactly on load)
     uint32_t *key;
     int32_t *rank;       // atomic rank, later reused as dest (inverse permutation)
     int32_t *count;      // [nbins]

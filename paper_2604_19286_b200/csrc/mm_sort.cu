@@ -97,6 +97,25 @@ __device__ __forceinline__ void load_vec3x4(const double *__restrict__ a, int64_
     }
 }
 
+// FP32 variant (mixed-precision inputs): three 16-B loads, widened exactly.
+template <bool VEC>
+__device__ __forceinline__ void load_vec3x4(const float *__restrict__ a, int64_t p0, int64_t np, double v[12])
+{
+    if (VEC && p0 + 4 <= np) {
+        const float4 *a4 = reinterpret_cast<const float4 *>(a + 3 * p0);
+        const float4 x = __ldg(a4), y = __ldg(a4 + 1), z = __ldg(a4 + 2);
+        v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+        v[4] = y.x; v[5] = y.y; v[6] = y.z; v[7] = y.w;
+        v[8] = z.x; v[9] = z.y; v[10] = z.z; v[11] = z.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int m = 0; m < 3; ++m)
+                v[3 * j + m] = (p0 + j < np) ? (double)a[3 * (p0 + j) + m] : 0.0;
+    }
+}
+
 __device__ __forceinline__ uint32_t bin_of(const Geo &g, const Located &L)
 {
     int32_t b[3];
@@ -116,7 +135,8 @@ __device__ __forceinline__ uint32_t bin_of(const Geo &g, const Located &L)
 // this removes the same-address atomic serialisation, and the ranks follow the particle index
 // inside each run (the per-bin fix-up then finds most slices already ascending).  On shuffled
 // input every lane is its own run (one atomic each, as before).
-__global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const double *__restrict__ pos,
+template <typename TP>
+__global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__restrict__ pos,
                                                 uint32_t *__restrict__ key, int32_t *__restrict__ rank,
                                                 int32_t *__restrict__ count, int32_t *__restrict__ status)
 {
@@ -130,7 +150,7 @@ __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const double 
         const int64_t p = base + 32 * j + lane;
 #pragma unroll
         for (int m = 0; m < 3; ++m)
-            x[j][m] = p < np ? __ldg(pos + 3 * p + m) : 0.0;
+            x[j][m] = p < np ? (double)__ldg(pos + 3 * p + m) : 0.0;
     }
     int err = 0;
     const unsigned below = (2u << lane) - 1u;  // lanes <= lane
@@ -502,9 +522,9 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
     }
 }
 
-template <bool VEC>
-__global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const double *__restrict__ pos, const double *__restrict__ q,
-                          const double *__restrict__ B, const uint32_t *__restrict__ key,
+template <bool VEC, typename TP>
+__global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP *__restrict__ pos, const double *__restrict__ q,
+                          const TP *__restrict__ B, const uint32_t *__restrict__ key,
                           const int32_t *__restrict__ dest, double *__restrict__ rec,
                           int32_t *__restrict__ status)
 {
@@ -628,7 +648,12 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
 
     if (b.np > 0) {
-        k_key<<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, b.status);
+        if (b.f32)
+            k_key<float><<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(
+                geo, b.np, reinterpret_cast<const float *>(b.pos), b.key, b.rank, b.count, b.status);
+        else
+            k_key<double><<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank,
+                                                                              b.count, b.status);
         count_launch();
         pt.mark("key");
     }
@@ -669,12 +694,19 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         count_launch();
     }
     if (b.np > 0) {
-        if (vec)
-            k_scatter<true><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
-                                                                      b.rec, b.status);
-        else
-            k_scatter<false><<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank,
-                                                                       b.rec, b.status);
+        const unsigned gs = blocks_for((b.np + 3) / 4, T);
+        if (b.f32) {
+            const float *pf = reinterpret_cast<const float *>(b.pos), *bf = reinterpret_cast<const float *>(b.B);
+            const bool v16 = ((uintptr_t)pf % 16 == 0) && ((uintptr_t)bf % 16 == 0) && ((uintptr_t)b.q % 32 == 0);
+            if (v16)
+                k_scatter<true, float><<<gs, T, 0, s>>>(geo, b.np, pf, b.q, bf, b.key, b.rank, b.rec, b.status);
+            else
+                k_scatter<false, float><<<gs, T, 0, s>>>(geo, b.np, pf, b.q, bf, b.key, b.rank, b.rec, b.status);
+        } else if (vec) {
+            k_scatter<true, double><<<gs, T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.rec, b.status);
+        } else {
+            k_scatter<false, double><<<gs, T, 0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.rec, b.status);
+        }
         count_launch();
         pt.mark("scatter");
     }

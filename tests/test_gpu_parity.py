@@ -474,3 +474,27 @@ def test_sort_scalar_handle_records(order):
             m.mm_assemble(hh, 1, prec, m.Species(), out)
             torch.cuda.synchronize()
             assert rel_err(out.cpu().numpy().astype(np.float64), ref) <= tol
+
+
+# ------------------------------------------------------------- mixed-precision inputs (NEXT-2)
+@pytest.mark.parametrize("order", [1, 2])
+def test_mixed_precision_inputs(order):
+    # FP32 positions and B, FP64 charges: the sort and the FP64 assembly equal the
+    # oracle run on the exactly widened arrays (sort bit-exact, entries <= 1e-12)
+    m = mm()
+    n = (7, 6, 5)
+    d = synth.particles(synth.Config("t", n, order, "tensor", 20, seed=41))
+    pos32, B32 = d["pos"].astype(np.float32), d["B"].astype(np.float32)
+    pos32 = np.where(np.floor(pos32.astype(np.float64)) >= np.array(n), 0.0, pos32).astype(np.float32)
+    w = {"pos": pos32.astype(np.float64), "q": d["q"], "B": B32.astype(np.float64)}
+    g = m.Grid(n)
+    h = m.mm_sort_by_cell(g, order, 4, torch.from_numpy(pos32).cuda(), torch.from_numpy(d["q"]).cuda(),
+                          torch.from_numpy(B32).cuda())
+    v = m.mm_sorted_view(h)
+    r = oracle.sort(n, order, 4, w["pos"], w["q"], w["B"])
+    assert (v["perm"].cpu().numpy() == r["perm"]).all()
+    assert (v["rec"].cpu().numpy().view(np.uint64) == r["rec"].view(np.uint64)).all()
+    out = torch.full(m.out_shape(g, order, 9), float("nan"), dtype=torch.float64, device="cuda")
+    m.mm_assemble(h, 9, m.MM_FP64, m.Species(), out)
+    torch.cuda.synchronize()
+    assert rel_err(out.cpu().numpy(), run_oracle(n, order, 9, w)) <= TOL
