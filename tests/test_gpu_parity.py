@@ -498,3 +498,35 @@ def test_mixed_precision_inputs(order):
     m.mm_assemble(h, 9, m.MM_FP64, m.Species(), out)
     torch.cuda.synchronize()
     assert rel_err(out.cpu().numpy(), run_oracle(n, order, 9, w)) <= TOL
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_c4_full_size_sampled_planes(order):
+    # config c4 at full size (128^3, clustered, 134.7 M particles drawn on the device as bench.py
+    # does), scalar kind, FP64 and (order 2) TF32: sampled node planes against the oracle run on
+    # the particles that can reach them
+    m = mm()
+    cfg = synth.config("c4o1")
+    d = synth.particles_device(cfg, "cuda", with_B=False)
+    n = cfg.n
+    g = m.Grid(n)
+    h = m.mm_sort_by_cell(g, order, 4, d["pos"], d["q"], None)
+    S = (2 * order + 1) ** 3
+    plane = n[1] * n[2]
+    precs = [(m.MM_FP64, torch.float64, TOL)] + ([(m.MM_TF32, torch.float32, 2e-3)] if order == 2 else [])
+    outs = []
+    for prec, dt, tol in precs:
+        out = torch.empty(m.out_shape(g, order, 1), dtype=dt, device="cuda")
+        m.mm_assemble(h, 1, prec, m.Species(), out)
+        outs.append((out.view(n[0], plane, S), tol))
+    torch.cuda.synchronize()
+    cx = torch.floor(d["pos"][:, 0]).long()
+    for X in (0, 37):
+        sel = torch.zeros_like(cx, dtype=torch.bool)
+        for c in range(X - order - 1, X + order + 1):
+            sel |= cx == (c % n[0])
+        sub = {"pos": d["pos"][sel].cpu().numpy(), "q": d["q"][sel].cpu().numpy(), "B": None}
+        ref = oracle.assemble(n, order, 1, sub["pos"], sub["q"]).reshape(n[0], plane, S)[X]
+        for o, tol in outs:
+            got = o[X].cpu().numpy().astype(np.float64)
+            assert rel_err(got[:, :, None], ref[:, :, None]) <= tol, (X, tol)
