@@ -154,30 +154,38 @@ __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__r
     }
     int err = 0;
     const unsigned below = (2u << lane) - 1u;  // lanes <= lane
+    uint32_t k[4];
+    int h[4], len[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         const int64_t p = base + 32 * j + lane;
-        uint32_t k = 0xffffffffu;
+        k[j] = 0xffffffffu;
         if (p < np) {
             Located L = locate(g, x[j][0], x[j][1], x[j][2]);
             if (L.err)
                 err |= L.err;
             else
-                k = bin_of(g, L);
+                k[j] = bin_of(g, L);
         }
-        const uint32_t kp = __shfl_up_sync(0xffffffffu, k, 1);
-        const bool head = lane == 0 || k != kp;
+        const uint32_t kp = __shfl_up_sync(0xffffffffu, k[j], 1);
+        const bool head = lane == 0 || k[j] != kp;
         const unsigned heads = __ballot_sync(0xffffffffu, head);
-        const int h = 31 - __clz(heads & below);                 // this lane's run head
+        h[j] = 31 - __clz(heads & below);                         // this lane's run head
         const unsigned after = heads & ~below;                    // heads past this lane
-        const int next = after ? __ffs(after) - 1 : 32;
-        int r = 0;
-        if (head && k != 0xffffffffu)
-            r = atomicAdd(&count[k], next - lane);               // run length (lanes lane..next-1)
-        r = __shfl_sync(0xffffffffu, r, h) + (lane - h);
+        len[j] = head ? (after ? __ffs(after) - 1 : 32) - lane : 0;  // run length (heads only)
+    }
+    // the four rounds' atomics are independent: issue them all before using any result
+    int r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        r[j] = (len[j] > 0 && k[j] != 0xffffffffu) ? atomicAdd(&count[k[j]], len[j]) : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t p = base + 32 * j + lane;
+        const int rr = __shfl_sync(0xffffffffu, r[j], h[j]) + (lane - h[j]);
         if (p < np) {
-            key[p] = k;
-            rank[p] = r;
+            key[p] = k[j];
+            rank[p] = rr;
         }
     }
     if (err)
