@@ -135,18 +135,20 @@ __device__ __forceinline__ uint32_t bin_of(const Geo &g, const Located &L)
 // this removes the same-address atomic serialisation, and the ranks follow the particle index
 // inside each run (the per-bin fix-up then finds most slices already ascending).  On shuffled
 // input every lane is its own run (one atomic each, as before).
+constexpr int KEY_R = 4;  // rounds of 32 particles per warp (8 spills and is slower on shuffled input)
+
 template <typename TP>
 __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__restrict__ pos,
                                                 uint32_t *__restrict__ key, int32_t *__restrict__ rank,
                                                 int32_t *__restrict__ count, int32_t *__restrict__ status)
 {
     const int lane = threadIdx.x & 31;
-    const int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * 128;
+    const int64_t base = ((int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)) * (32 * KEY_R);
     if (base >= np)
         return;
-    double x[4][3];
+    double x[KEY_R][3];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < KEY_R; ++j) {
         const int64_t p = base + 32 * j + lane;
 #pragma unroll
         for (int m = 0; m < 3; ++m)
@@ -154,10 +156,10 @@ __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__r
     }
     int err = 0;
     const unsigned below = (2u << lane) - 1u;  // lanes <= lane
-    uint32_t k[4];
-    int h[4], len[4];
+    uint32_t k[KEY_R];
+    int h[KEY_R], len[KEY_R];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < KEY_R; ++j) {
         const int64_t p = base + 32 * j + lane;
         k[j] = 0xffffffffu;
         if (p < np) {
@@ -174,13 +176,13 @@ __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__r
         const unsigned after = heads & ~below;                    // heads past this lane
         len[j] = head ? (after ? __ffs(after) - 1 : 32) - lane : 0;  // run length (heads only)
     }
-    // the four rounds' atomics are independent: issue them all before using any result
-    int r[4];
+    // the rounds' atomics are independent: issue them all before using any result
+    int r[KEY_R];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < KEY_R; ++j)
         r[j] = (len[j] > 0 && k[j] != 0xffffffffu) ? atomicAdd(&count[k[j]], len[j]) : 0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < KEY_R; ++j) {
         const int64_t p = base + 32 * j + lane;
         const int rr = __shfl_sync(0xffffffffu, r[j], h[j]) + (lane - h[j]);
         if (p < np) {
@@ -657,10 +659,10 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
 
     if (b.np > 0) {
         if (b.f32)
-            k_key<float><<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(
+            k_key<float><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(
                 geo, b.np, reinterpret_cast<const float *>(b.pos), b.key, b.rank, b.count, b.status);
         else
-            k_key<double><<<blocks_for((b.np + 127) / 128 * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank,
+            k_key<double><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank,
                                                                               b.count, b.status);
         count_launch();
         pt.mark("key");
