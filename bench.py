@@ -681,11 +681,34 @@ def main():
             tt = T.tensor([ems], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
-        h2d = sum(v.numel() * v.element_size() for v in hp.values())
-        line["e2e"] = {"value": r1["np"] * world * ke / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        h2d_bytes = sum(v.numel() * v.element_size() for v in hp.values())
+        line["e2e"] = {"value": r1["np"] * world * ke / (ems / 1e3) / 1e6, "unit": UNIT,
+                       "h2d_bytes_per_step": h2d_bytes,
                        "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke,
                        "note": "pinned host pos/q/B -> device, sort + assemble, full mass matrix -> pinned host; "
                                "pipelined across steps (H2D of k+1 and D2H of k-1 overlap step k)"}
+        # the same end-to-end pipeline with the production storage of PAPER.md:576 (FP32 positions
+        # and B, mm_sort_by_cell_mixed): half the H2D bytes of the inputs
+        if world == 1 and "mixed_inputs" in line:
+            p32 = d["pos"].astype(np.float32)
+            L32 = np.array(cfg.n, dtype=np.float32)
+            p32 = np.where(p32 >= L32, p32 - L32, p32)
+            hp = {"pos": T.from_numpy(p32).pin_memory(), "q": hp["q"],
+                  "B": T.from_numpy(d["B"].astype(np.float32)).pin_memory()}
+            dds[0] = {k: T.empty(v.shape, dtype=v.dtype, device=dev) for k, v in hp.items()}
+            dds[1] = {k: T.empty_like(v) for k, v in dds[0].items()}
+            hs[0], hs[1] = None, None
+            ev_d2h[0] = ev_d2h[1] = None
+            run_e2e(2)
+            T.cuda.synchronize()
+            e0.record(s_h2d)
+            run_e2e(ke)
+            e1.record(s_d2h)
+            T.cuda.synchronize()
+            ems_m = e0.elapsed_time(e1)
+            line["mixed_inputs"]["e2e"] = {"value": r1["np"] * ke / (ems_m / 1e3) / 1e6, "unit": UNIT,
+                                           "h2d_bytes_per_step": sum(v.numel() * v.element_size() for v in hp.values()),
+                                           "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke}
 
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = oracle_rate(cfg, r1["d"])
