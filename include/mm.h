@@ -199,6 +199,26 @@ mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, c
                    int accumulate, void *stream);
 
 /*
+ * mm_slab_partition — particle migration between x-slabs, the first half of the "sort &
+ * communicate" stage: a STABLE 3-way partition of a
+ * rank's particles by the slab of their cell along x (cell = floor(x/h), IEEE quotient, R5):
+ *   class 0: stays      (cell in [x_begin, x_end))
+ *   class 1: to r - 1   (leaves through x_begin)
+ *   class 2: to r + 1   (leaves through x_end)
+ * The cells outside the slab are split half-and-half between the two directions (periodic),
+ * so particles may move up to half the remaining domain.  Non-finite or out-of-domain
+ * positions are kept in class 0 (mm_sort_by_cell reports them).
+ *   g          host, grid with this rank's slab
+ *   pos,q,B    device, FP64 [np][3], [np], [np][3] (B may be NULL)
+ *   pos_out,q_out,B_out  device, same shapes: [class 0 | class 1 | class 2], input order kept
+ *              inside every class; must not alias the inputs
+ *   counts     host int64[3]: particles per class
+ * Synchronous (waits for `stream` to read the counts back).
+ */
+mm_status mm_slab_partition(const mm_grid *g, int64_t np, const double *pos, const double *q, const double *B,
+                            double *pos_out, double *q_out, double *B_out, int64_t counts[3], void *stream);
+
+/*
  * mm_ghost_add — add `nplanes` received ghost node planes into owned rows (FP64 output)
  * (the reduction step of the slab decomposition):
  *   out[((first_plane + k)*n1*n2 + r)*S*C + e] += recv[(k*n1*n2 + r)*S*C + e]

@@ -32,7 +32,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
                  4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
+EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_slab_partition", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
            "mm_out_elems", "mm_free", "mm_last_error", "mm_version", "mm_launch_count"]
 
 
@@ -82,6 +82,8 @@ def load_library(build_if_missing: bool = True):
     lib.mm_assemble.argtypes = [P, I, I, P, I, P, P, P]
     lib.mm_assemble.restype = I
     lib.mm_ghost_add.argtypes = [P, I, I, P, P, I, I, P]
+    lib.mm_slab_partition.restype = I
+    lib.mm_slab_partition.argtypes = [P, I64, P, P, P, P, P, P, P, P]
     lib.mm_apply.restype = I
     lib.mm_apply.argtypes = [P, I, I, P, P, P, I, P]
     lib.mm_ghost_add.restype = I
@@ -238,6 +240,21 @@ def mm_apply(grid: mm_grid, order: int, kind: int, M, E, y, accumulate: bool = F
     lib = load_library()
     _check(lib.mm_apply(ctypes.byref(grid), int(order), int(kind), _dev_ptr(M, name="M"), _dev_ptr(E, name="E"),
                         _dev_ptr(y, name="y"), int(bool(accumulate)), _stream_ptr(stream)))
+
+
+def mm_slab_partition(grid: mm_grid, pos, q, B=None, stream=None):
+    """Stable partition of a rank's particles into (stay, to r-1, to r+1) by their slab
+    (include/mm.h).  Returns (pos_out, q_out, B_out, counts) with the classes concatenated."""
+    lib = load_library()
+    np_ = int(pos.shape[0])
+    pos_o, q_o = torch.empty_like(pos), torch.empty_like(q)
+    B_o = torch.empty_like(B) if B is not None else None
+    counts = (ctypes.c_int64 * 3)()
+    _check(lib.mm_slab_partition(ctypes.byref(grid), np_, _dev_ptr(pos, name="pos"), _dev_ptr(q, name="q"),
+                                 _dev_ptr(B, name="B") if B is not None else None, _dev_ptr(pos_o, name="pos_out"),
+                                 _dev_ptr(q_o, name="q_out"), _dev_ptr(B_o, name="B_out") if B is not None else None,
+                                 counts, _stream_ptr(stream)))
+    return pos_o, q_o, B_o, (int(counts[0]), int(counts[1]), int(counts[2]))
 
 
 def mm_free(handle: Sorted):

@@ -419,6 +419,42 @@ mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, c
     }
 }
 
+mm_status mm_slab_partition(const mm_grid *g, int64_t np, const double *pos, const double *q, const double *B,
+                            double *pos_out, double *q_out, double *B_out, int64_t counts[3], void *stream)
+{
+    try {
+        mm_status st = check_grid(g, 1);
+        if (st)
+            return st;
+        if (!counts || np < 0 || np >= INT32_MAX)
+            return fail(MM_ERR_INVALID_ARG, "counts NULL or np out of range");
+        if (np > 0 && (!pos || !q || !pos_out || !q_out || (B && !B_out)))
+            return fail(MM_ERR_INVALID_ARG, "NULL particle arrays");
+        cudaStream_t s = (cudaStream_t)stream;
+        const mm::Geo geo = mm::make_geo(*g, 1);
+        int32_t *tmp = nullptr;
+        const int64_t nt = mm::partition_tmp_elems(np);
+        cudaError_t e = cudaMallocAsync((void **)&tmp, sizeof(int32_t) * (size_t)nt, s);
+        if (!e)
+            e = mm::partition_enqueue(geo, np, pos, q, B, pos_out, q_out, B_out, tmp, s);
+        int32_t ends[3] = {0, 0, 0};
+        if (!e)
+            e = cudaMemcpyAsync(ends, tmp + nt - 3, sizeof(ends), cudaMemcpyDeviceToHost, s);
+        if (tmp)
+            cudaFreeAsync(tmp, s);
+        if (!e)
+            e = cudaStreamSynchronize(s);
+        if (e)
+            return cuda_fail(e, "mm_slab_partition");
+        counts[0] = ends[0];
+        counts[1] = ends[1] - ends[0];
+        counts[2] = ends[2] - ends[1];
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_slab_partition");
+    }
+}
+
 mm_status mm_ghost_add(const mm_grid *g, int order, mm_kind kind, double *out, const double *recv, int first_plane,
                        int nplanes, void *stream)
 {

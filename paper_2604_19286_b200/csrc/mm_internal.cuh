@@ -77,5 +77,9 @@ cudaError_t apply_enqueue(const Geo &geo, int ncomp, const double *M, const doub
 
 // ---- halo (mm_halo.cu) -----------------------------------------------------
 cudaError_t ghost_add_enqueue(double *out, const double *recv, int64_t n, cudaStream_t s);
+int64_t partition_tmp_elems(int64_t np);
+// tmp: [partition_tmp_elems(np)] int32; the class ends are left in tmp[3 ntiles .. +2]
+cudaError_t partition_enqueue(const Geo &g, int64_t np, const double *pos, const double *q, const double *B,
+                              double *pos_o, double *q_o, double *B_o, int32_t *tmp, cudaStream_t s);
 
 }  // namespace mm

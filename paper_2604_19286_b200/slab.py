@@ -66,3 +66,54 @@ def exchange_ghosts(out: torch.Tensor, ghost: torch.Tensor, order: int, plane_el
     for k in range(len(send_prev)):
         add(widths[rank] - 1 - k, recv_from_next[k])
     return out
+
+
+def migrate(pos: torch.Tensor, q: torch.Tensor, B, rank: int, world: int, partition, group=None):
+    """Send the particles that left this rank's slab to the slab neighbours (periodic ring) and
+    return this rank's new (pos, q, B): [stayed | received from r-1 | received from r+1].
+
+    The "sort & communicate" stage of the PIC cycle: after
+    the mover, particles are owned by cell again before mm_sort_by_cell.
+    partition(pos, q, B) -> (pos_o, q_o, B_o, (n_stay, n_prev, n_next)): the stable 3-way
+    partition (mm_slab_partition on GPUs; a torch stand-in in the CPU tests).
+    Messages per step: the two leaver counts, then the packed leavers [n, 7] (or [n, 4] without
+    B) to each neighbour, posted in the same order as exchange_ghosts (next first)."""
+    pos_o, q_o, B_o, (ns, npv, nnx) = partition(pos, q, B)
+    if world == 1:
+        return pos_o, q_o, B_o
+    nxt, prv = (rank + 1) % world, (rank - 1) % world
+
+    def pack(a, b):
+        cols = [pos_o[a:b], q_o[a:b, None]] + ([B_o[a:b]] if B_o is not None else [])
+        return torch.cat(cols, dim=1).contiguous()
+
+    to_prev, to_next = pack(ns, ns + npv), pack(ns + npv, ns + npv + nnx)
+    dev = pos.device
+    c_next = torch.tensor([nnx], dtype=torch.int64, device=dev)
+    c_prev = torch.tensor([npv], dtype=torch.int64, device=dev)
+    r_prev = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r-1 (its to_next)
+    r_next = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r+1 (its to_prev)
+    ops = [dist.P2POp(dist.isend, c_next, nxt, group), dist.P2POp(dist.irecv, r_prev, prv, group),
+           dist.P2POp(dist.isend, c_prev, prv, group), dist.P2POp(dist.irecv, r_next, nxt, group)]
+    for req in dist.batch_isend_irecv(ops):
+        req.wait()
+    ncol = to_next.shape[1]
+    from_prev = torch.empty((int(r_prev.item()), ncol), dtype=pos.dtype, device=dev)
+    from_next = torch.empty((int(r_next.item()), ncol), dtype=pos.dtype, device=dev)
+    ops = []
+    if nnx:
+        ops.append(dist.P2POp(dist.isend, to_next, nxt, group))
+    if from_prev.shape[0]:
+        ops.append(dist.P2POp(dist.irecv, from_prev, prv, group))
+    if npv:
+        ops.append(dist.P2POp(dist.isend, to_prev, prv, group))
+    if from_next.shape[0]:
+        ops.append(dist.P2POp(dist.irecv, from_next, nxt, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    got = torch.cat([from_prev, from_next], dim=0)
+    new_pos = torch.cat([pos_o[:ns], got[:, 0:3]], dim=0).contiguous()
+    new_q = torch.cat([q_o[:ns], got[:, 3]], dim=0).contiguous()
+    new_B = torch.cat([B_o[:ns], got[:, 4:7]], dim=0).contiguous() if B_o is not None else None
+    return new_pos, new_q, new_B

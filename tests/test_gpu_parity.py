@@ -530,3 +530,29 @@ def test_c4_full_size_sampled_planes(order):
         for o, tol in outs:
             got = o[X].cpu().numpy().astype(np.float64)
             assert rel_err(got[:, :, None], ref[:, :, None]) <= tol, (X, tol)
+
+
+# ------------------------------------------------------------- slab migration (NEXT-1)
+@pytest.mark.parametrize("xb,xe", [(0, 16), (5, 9), (12, 16), (0, 3)])
+def test_slab_partition(xb, xe):
+    # stable 3-way partition by slab (include/mm.h): classes and order against numpy
+    m = mm()
+    n = (16, 6, 7)
+    rng = np.random.default_rng(xb * 31 + xe)
+    npart = 50000
+    pos = rng.random((npart, 3)) * np.array(n)
+    pos = np.where(pos >= np.array(n), 0.0, pos)
+    qq = rng.uniform(-1, 1, npart)
+    B = rng.uniform(-1, 1, (npart, 3))
+    g = m.Grid(n, (1.0, 1.0, 1.0), xb, xe)
+    po, qo, Bo, cnt = m.mm_slab_partition(g, torch.from_numpy(pos).cuda(), torch.from_numpy(qq).cuda(),
+                                          torch.from_numpy(B).cuda())
+    c = np.floor(pos[:, 0]).astype(int)
+    u = (c - xb) % n[0]
+    w = xe - xb
+    cls = np.where(u < w, 0, np.where((u - w) < (n[0] - w + 1) // 2, 2, 1))
+    idx = np.concatenate([np.nonzero(cls == k)[0] for k in range(3)])
+    assert cnt == tuple(int((cls == k).sum()) for k in range(3))
+    assert (po.cpu().numpy() == pos[idx]).all()
+    assert (qo.cpu().numpy() == qq[idx]).all()
+    assert (Bo.cpu().numpy() == B[idx]).all()

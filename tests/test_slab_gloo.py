@@ -84,3 +84,60 @@ def test_slab_bounds_cover():
             b = [slab.slab_bounds(n0, w, r) for r in range(w)]
             assert b[0][0] == 0 and b[-1][1] == n0
             assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+
+
+# ------------------------------------------------------------- particle migration (NEXT-1)
+def partition_reference(n0, h, xb, xe):
+    """Stable 3-way partition by slab (the rule of include/mm.h mm_slab_partition), in torch."""
+    def part(pos, q, B):
+        c = torch.floor(pos[:, 0] / h).long()
+        u = (c - xb) % n0
+        w = xe - xb
+        cls = torch.where(u < w, 0, torch.where((u - w) < (n0 - w + 1) // 2, 2, 1))
+        idx = torch.cat([torch.nonzero(cls == k).flatten() for k in range(3)])
+        cnt = tuple(int((cls == k).sum()) for k in range(3))
+        return pos[idx], q[idx], (B[idx] if B is not None else None), cnt
+    return part
+
+
+def _migrate_worker(rank, world, port, n, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        cfg = synth.Config("t", n, 1, "tensor", 4, seed=33)
+        xb, xe = slab.slab_bounds(n[0], world, rank)
+        d = synth.particles(cfg, xb, xe)
+        # the mover: every particle displaced by up to 1.5 cells along x (periodic)
+        rng = np.random.default_rng(100 + rank)
+        pos = d["pos"].copy()
+        pos[:, 0] = (pos[:, 0] + rng.uniform(-1.5, 1.5, len(pos))) % n[0]
+        pos[:, 0] = np.where(pos[:, 0] >= n[0], 0.0, pos[:, 0])
+        t = {k: torch.from_numpy(v) for k, v in (("pos", pos), ("q", d["q"]), ("B", d["B"]))}
+        p2, q2, B2 = slab.migrate(t["pos"], t["q"], t["B"], rank, world, partition_reference(n[0], 1.0, xb, xe))
+        q.put((rank, xb, xe, p2.numpy(), q2.numpy(), B2.numpy(), pos, d["q"], d["B"]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_slab_migration_gloo(world):
+    n = (12, 4, 5)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    before = np.concatenate([np.column_stack([r[6], r[7], r[8]]) for r in res])
+    after = np.concatenate([np.column_stack([r[3], r[4], r[5]]) for r in res])
+    # particles owned by cell after the exchange, none lost or duplicated (rows as multisets)
+    for rank, xb, xe, p2, q2, B2, *_ in res:
+        cx = np.floor(p2[:, 0]).astype(int)
+        assert ((cx >= xb) & (cx < xe)).all(), rank
+    key = lambda a: a[np.lexsort(a.T[::-1])]
+    assert after.shape == before.shape
+    assert (key(after) == key(before)).all()
