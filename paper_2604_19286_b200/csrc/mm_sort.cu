@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(256, 4) k_key(Geo g, int64_t np, const TP *__r
         const int rr = __shfl_sync(0xffffffffu, r[j], h[j]) + (lane - h[j]);
         if (p < np) {
             key[p] = k[j];
-            rank[p] = rr;
+            rank[p] = k[j] != 0xffffffffu ? rr : -1;  // -1: no bin (the call fails), no record
         }
     }
     if (err)
@@ -530,8 +530,7 @@ __global__ void __launch_bounds__(1024) k_fix_huge(int64_t np, const uint32_t *_
 
 template <bool VEC, typename TP>
 __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP *__restrict__ pos, const double *__restrict__ q,
-                          const TP *__restrict__ B, const uint32_t *__restrict__ key,
-                          const int32_t *__restrict__ dest, double *__restrict__ rec,
+                          const TP *__restrict__ B, const int32_t *__restrict__ dest, double *__restrict__ rec,
                           int32_t *__restrict__ status)
 {
     extern __shared__ __align__(128) double sm_rec[];  // [256 threads][4 records][8]
@@ -539,20 +538,15 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP 
     if (p0 >= np)
         return;
     const bool full = p0 + 4 <= np;
-    uint32_t k[4];
-    int d[4];
+    int d[4];  // sorted slot of each particle; -1 for a particle without a bin (failed locate)
     double qq[4], x[12], bb[12];
     if (full) {
-        uint4 kk = *reinterpret_cast<const uint4 *>(key + p0);
         int4 dd = *reinterpret_cast<const int4 *>(dest + p0);
-        k[0] = kk.x; k[1] = kk.y; k[2] = kk.z; k[3] = kk.w;
         d[0] = dd.x; d[1] = dd.y; d[2] = dd.z; d[3] = dd.w;
     } else {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            k[j] = p0 + j < np ? key[p0 + j] : 0xffffffffu;
-            d[j] = p0 + j < np ? dest[p0 + j] : 0;
-        }
+        for (int j = 0; j < 4; ++j)
+            d[j] = p0 + j < np ? dest[p0 + j] : -1;
     }
     load_vec3x4<VEC>(pos, p0, np, x);
     if (VEC && full) {
@@ -573,7 +567,7 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP 
     int err = 0;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-        if (k[j] == 0xffffffffu)
+        if (d[j] < 0)
             continue;
         Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
         if (!(isfinite(qq[j]) && isfinite(bb[3 * j]) && isfinite(bb[3 * j + 1]) && isfinite(bb[3 * j + 2])))
@@ -739,14 +733,14 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
             const float *pf = reinterpret_cast<const float *>(b.pos), *bf = reinterpret_cast<const float *>(b.B);
             const bool v16 = ((uintptr_t)pf % 16 == 0) && ((uintptr_t)bf % 16 == 0) && ((uintptr_t)b.q % 32 == 0);
             if (v16)
-                k_scatter<true, float><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, pf, b.q, bf, b.key, b.rank, b.rec, b.status);
+                k_scatter<true, float><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, pf, b.q, bf, b.rank, b.rec, b.status);
             else
-                k_scatter<false, float><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, pf, b.q, bf, b.key, b.rank, b.rec,
+                k_scatter<false, float><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, pf, b.q, bf, b.rank, b.rec,
                                                                  b.status);
         } else if (vec) {
-            k_scatter<true, double><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.rec, b.status);
+            k_scatter<true, double><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, b.pos, b.q, b.B, b.rank, b.rec, b.status);
         } else {
-            k_scatter<false, double><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.rec,
+            k_scatter<false, double><<<gs, T, SCAT_SMEM, s>>>(geo, b.np, b.pos, b.q, b.B, b.rank, b.rec,
                                                               b.status);
         }
         count_launch();
