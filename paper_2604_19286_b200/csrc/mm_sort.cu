@@ -364,6 +364,71 @@ __device__ __forceinline__ void bitonic_reg(int32_t &v0, int32_t &v1, int lane)
 }
 
 // pad slots: perm -1, all-zero records (rs = record stride in doubles: 8 with B, 4 without)
+// Register bitonic network over K = 32 R keys, element i = lane + 32 r in v[r]: partners at
+// distance j >= 32 sit in the same lane (register r ^ j/32), at j < 32 in lane ^ j (shuffle).
+// Everything is unrolled: partner distances, directions and register indices are constants.
+template <int R>
+__device__ __forceinline__ void bitonic_regs(int32_t (&v)[R], int lane)
+{
+    constexpr int K = 32 * R;
+#pragma unroll
+    for (int k = 2; k <= K; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & jr)
+                        continue;
+                    const int r2 = r | jr;
+                    const bool up = ((lane + 32 * r) & k) == 0;
+                    const int32_t lo = min(v[r], v[r2]), hi = max(v[r], v[r2]);
+                    v[r] = up ? lo : hi;
+                    v[r2] = up ? hi : lo;
+                }
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int32_t pv = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool up = ((lane + 32 * r) & k) == 0;
+                    v[r] = (lower == up) ? min(v[r], pv) : max(v[r], pv);
+                }
+            }
+        }
+    }
+}
+
+// A bin of 64 < n <= 32 R particles held in registers: skip the network when the slice is
+// already ascending, then write perm and the inverse permutation.
+template <int R>
+__device__ __forceinline__ void fix_bin_regs(int32_t *__restrict__ perm, int32_t *__restrict__ dest, int64_t b, int n,
+                                             int lane)
+{
+    int32_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        v[r] = lane + 32 * r < n ? perm[b + lane + 32 * r] : INT_MAX;
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int32_t nx = __shfl_down_sync(0xffffffffu, v[r], 1);
+        const int32_t first = r + 1 < R ? __shfl_sync(0xffffffffu, v[r + 1 < R ? r + 1 : r], 0) : INT_MAX;
+        ok = ok && (lane < 31 ? v[r] <= nx : v[r] <= first);
+    }
+    if (!__all_sync(0xffffffffu, ok))
+        bitonic_regs<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        if (i < n) {
+            perm[b + i] = v[r];
+            dest[v[r]] = (int32_t)(b + i);
+        }
+    }
+}
+
 __device__ __forceinline__ void zero_pads(int32_t *perm, double *rec, int rs, int64_t from, int64_t to, int tid,
                                           int nthr)
 {
@@ -426,6 +491,15 @@ __global__ void __launch_bounds__(FIX_WARPS * 32) k_fix_warp(int64_t nbins, cons
                 perm[b + lane + 32] = v1;
                 dest[v1] = (int32_t)(b + lane + 32);
             }
+            continue;
+        }
+        if (n <= 512) {  // register networks (the shared-memory network below is slower)
+            if (n <= 128)
+                fix_bin_regs<4>(perm, dest, b, n, lane);
+            else if (n <= 256)
+                fix_bin_regs<8>(perm, dest, b, n, lane);
+            else
+                fix_bin_regs<16>(perm, dest, b, n, lane);
             continue;
         }
         int N = 32;
