@@ -20,8 +20,8 @@
 // 8 warps per CTA: each bin has 2 (order 1) or 4 (order 2) warps that split its X / Z rows in
 // the prep and its entries in the deposit; warps 0-3 read the accumulators (lane quarter = warp).
 // Per 32-particle chunk: prep (FP32 from the FP64 record; the support base is decided in FP64
-// exactly as in the sort) -> staging [row][particle] -> TF32 (cvt.rna) K-major tiles (no-swizzle
-// canonical layout: 8-row x 16-B core matrices, LBO = 128 B, SBO = 256 B) in a double buffer ->
+// exactly as in the sort), rounded to TF32 and stored straight into 128-B-swizzled K-major tiles
+// (one 128-B row per M / N row; conflict-free for lane = particle) in a double buffer ->
 // one thread issues 4 K-steps (x3 for 3xTF32: D += Ah Bh + Ah Bl + Al Bh) and commits to the
 // buffer's mbarrier.  Epilogue per group: tcgen05.ld -> staged block -> FP32 REDs in global
 // address order (the FP64 kernels' deposit tables).
@@ -68,12 +68,14 @@ __device__ __forceinline__ float *row_ptr_f(const Geo &g, int X, int Y, int Z, f
 }
 
 // ---- UMMA descriptors --------------------------------------------------------
-// Shared-memory matrix descriptor, K-major, no swizzle (layout type 0), version 1.
-__device__ __forceinline__ uint64_t umma_desc(const void *base, uint32_t lbo, uint32_t sbo)
+// Shared-memory matrix descriptor, K-major, 128-B swizzle (layout type 2, version 1): rows of
+// 128 B (32 TF32 K-elements), 8-row atoms of 1024 B (SBO), 16-B chunk index XOR (row & 7);
+// the K-step start advances by 32 B inside the swizzled row.  Atoms 1024-B aligned.
+__device__ __forceinline__ uint64_t umma_desc_sw128(const void *base)
 {
     const uint64_t a = smem_u32(base);
-    return ((a >> 4) & 0x3FFFull) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-           ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46);
+    return ((a >> 4) & 0x3FFFull) | ((uint64_t)(16 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+           (2ull << 61);
 }
 
 // Instruction descriptor: D = F32, A = B = TF32, both K-major, M = 128, N.
@@ -204,20 +206,20 @@ struct PP {
     static constexpr int NB = ORDER == 1 ? 16 : 64;     // B (X) rows per bin
     static constexpr int N = BPC * NB;                  // MMA N: 64 | 128
     static_assert(NZ <= MB && NX <= NB, "bin block does not fit");
-    static constexpr int CH = 32, KS = CH / 8;          // particles per chunk, K-steps
+    static constexpr int CH = 32;                       // particles per chunk (4 K-steps of 8)
     static constexpr int PARTS = X3 ? 2 : 1;
-    static constexpr int A_STEP = 128 * 32, B_STEP = N * 32;            // bytes per K-step
-    static constexpr int PART_BYTES = KS * (A_STEP + B_STEP);
+    // operand tiles of a 32-particle chunk, K-major with 128-B swizzle: one 128-B row per M / N
+    // row (K = 32 TF32), A = 128 rows (16 KB), B = N rows
+    static constexpr int A_BYTES = 128 * 128, B_BYTES = N * 128;
+    static constexpr int PART_BYTES = A_BYTES + B_BYTES;
     static constexpr int BUF_BYTES = PARTS * PART_BYTES;
-    static constexpr int ROWS = NX + NZ;                // staging rows per bin (X then Z)
-    static constexpr int SS = 36;                       // staging row stride (floats)
+    static constexpr int ROWS = NX + NZ;                // operand rows per bin (X then Z)
     static constexpr int L = 2 * ORDER + 1, S = L * L * L, RL = S * NC;
     static constexpr int NDEP = 64 * NC;                // order-1 deposit entries per bin
     static constexpr int NUNIT = 81;                    // order-2 flush units (a, b_x)
     static constexpr int OFF_OP = 0;
-    static constexpr int OFF_STG = OFF_OP + 2 * BUF_BYTES;
-    static_assert(NX * NZ <= ROWS * SS, "the epilogue block aliases the slot's staging");
-    static constexpr int OFF_TAB = OFF_STG + BPC * ROWS * SS * 4;
+    static constexpr int OFF_STG = OFF_OP + 2 * BUF_BYTES;  // epilogue blocks [BPC][NX][NZ]
+    static constexpr int OFF_TAB = OFF_STG + (BPC * NX * NZ * 4 + 15) / 16 * 16;
     static constexpr bool OT = ORDER == 2 && NC == 1;  // order-2 scalar: table deposit (runs of 3 are too short)
     static constexpr int NDEP2 = 736;                   // 27 x 27 entries, padded to 32
     static constexpr int TAB_BYTES = ORDER == 1 ? NDEP * 4 : (OT ? NDEP2 * 4 : NUNIT * 16);
@@ -227,22 +229,26 @@ struct PP {
     static constexpr int TMEM_COLS = N;
 };
 
-// Prep of one warp's share [R0, R1) of a bin's staging rows (X rows, then Z rows; lane =
-// particle of the chunk, zeros past the bin's end), then the share's TF32 K-major tiles:
-// item = (row, 4 particles), 16-B stores.  Lanes 8q..8q+7 take 8 consecutive rows at K offset
-// 4q (and 4q + 16): distinct 16-B slots of the core matrices (conflict-free stores), staging
-// rows 4 banks apart (loads).  Only this warp reads its rows back: a __syncwarp suffices.
+// Prep of one warp's share [R0, R1) of a bin's operand rows (X rows, then Z rows; lane = particle
+// k of the chunk, zeros past the bin's end), written straight into the 128-B-swizzled K-major
+// tiles as TF32: element (row m, k) at (m >> 3) 1024 + (m & 7) 128 + ((k >> 2) ^ (m & 7)) 16 +
+// (k & 3) 4.  For a fixed row the 32 lanes hit 32 distinct banks (no staging round trip).
 template <int ORDER, int NC, bool X3, int ROLE>
-__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t stg_s, uint32_t op_s,
-                                          int pj, int lane, float fws, float fsig)
+__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t op_s, int pj,
+                                          int lane, float fws, float fsig)
 {
     using T = PP<ORDER, NC, X3>;
-    constexpr int R0 = ROLE * T::ROWS / T::WPB, R1 = (ROLE + 1) * T::ROWS / T::WPB;
-    if (ROLE >= T::WPB)
+    if constexpr (ROLE >= T::WPB) {
         return;
-    const uint32_t stg_lane = stg_s + 4 * lane;
+    } else {
+    constexpr int R0 = ROLE * T::ROWS / T::WPB, R1 = (ROLE + 1) * T::ROWS / T::WPB;
+    // lane part of the swizzled offset for each value of (row & 7)
+    uint32_t lo8[8];
+#pragma unroll
+    for (int r7 = 0; r7 < 8; ++r7)
+        lo8[r7] = (uint32_t)((((lane >> 2) ^ r7) << 4) + (lane & 3) * 4 + r7 * 128);
+    float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
     if (live) {
-        float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
         if (R0 < T::NX) {
             pair_products<ORDER>(ca.x, qx);
             pair_products<ORDER>(ca.y, qy);
@@ -251,61 +257,33 @@ __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, 
             pair_products<ORDER>(ca.z, qz);
             coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
         }
-#pragma unroll
-        for (int r = R0; r < R1; ++r) {
-            const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(v) : "memory");
-        }
-    } else {
-#pragma unroll
-        for (int r = R0; r < R1; ++r)
-            asm volatile("st.shared.f32 [%0], %1;" ::"r"(stg_lane + r * T::SS * 4), "f"(0.0f) : "memory");
     }
-    __syncwarp();
-    const int r8 = lane & 7, kq = lane >> 3;
 #pragma unroll
-    for (int g8 = R0; g8 < R1; g8 += 8) {
-        const int rr = g8 + r8;
-        if (rr < R1) {
-            const int trow = rr < T::NX ? T::NB * pj + rr : T::MB * pj + rr - T::NX;
-            const uint32_t dst = op_s + (rr < T::NX ? T::A_STEP : 0) + (trow >> 3) * 256 + (trow & 7) * 16 + (kq & 1) * 128;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float v[4];
-                asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
-                             : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3])
-                             : "r"(stg_s + (uint32_t)(rr * T::SS + 4 * (kq + 4 * h)) * 4));
-                uint32_t hi[4], lo[4];
-#pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    hi[t] = tf32_rna(v[t]);
-                    lo[t] = tf32_rna(v[t] - __uint_as_float(hi[t]));
-                }
-                const uint32_t d = dst + ((kq >> 1) + 2 * h) * (T::A_STEP + T::B_STEP);
-                asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d), "r"(hi[0]), "r"(hi[1]), "r"(hi[2]),
-                             "r"(hi[3])
-                             : "memory");
-                if (X3)
-                    asm volatile("st.shared.v4.b32 [%0], {%1,%2,%3,%4};" ::"r"(d + T::PART_BYTES), "r"(lo[0]),
-                                 "r"(lo[1]), "r"(lo[2]), "r"(lo[3])
-                                 : "memory");
-            }
-        }
+    for (int r = R0; r < R1; ++r) {
+        float v = 0.0f;
+        if (live)
+            v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
+        const int m = r < T::NX ? T::NB * pj + r : T::MB * pj + r - T::NX;   // tile row
+        const uint32_t d = op_s + (r < T::NX ? T::A_BYTES : 0) + (uint32_t)(m >> 3) * 1024 + lo8[m & 7];
+        const uint32_t hi = tf32_rna(v);
+        asm volatile("st.shared.b32 [%0], %1;" ::"r"(d), "r"(hi) : "memory");
+        if (X3)
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(d + T::PART_BYTES), "r"(tf32_rna(v - __uint_as_float(hi)))
+                         : "memory");
+    }
     }
 }
 
 template <int ORDER, int NC, bool X3>
-__global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__restrict__ rec,
+__global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, int rs,
                                                   double wscale, double sigma, float *__restrict__ out,
                                                   float *__restrict__ ghost)
 {
     using T = PP<ORDER, NC, X3>;
     extern __shared__ __align__(1024) unsigned char smem[];
-    float *stg = reinterpret_cast<float *>(smem + T::OFF_STG);   // [BPC][ROWS][SS]
-    // epi[pj] ([NX][NZ]) aliases slot pj's staging: it is written after the slot's last chunk
-    // barrier and read until the barrier that closes the deposit
-    float *epi = stg;
+    float *stg = reinterpret_cast<float *>(smem + T::OFF_STG);   // [BPC][NX][NZ] epilogue blocks
+    float *epi = stg;  // epi[pj]: slot pj's accumulators [NX][NZ], read by its deposit
     int *tab = reinterpret_cast<int *>(smem + T::OFF_TAB);
     float **rowp = reinterpret_cast<float **>(smem + T::OFF_ROWP);  // [BPC][32]
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + T::OFF_BAR);  // 3 BPC mbarriers
@@ -368,12 +346,12 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
     const uint32_t tmem = *s_taddr;
     const float fws = (float)wscale, fsig = (float)sigma;
 
-    // prep role of this warp: bin pj, an equal share [r0, r1) of its staging rows (X rows, then
+    // prep role of this warp: bin pj, an equal share [r0, r1) of its operand rows (X rows, then
     // Z rows).  order 1: bin j = warps j, 4+j; order 2: bin j = warps {2j, 2j+1, 2j+4, 2j+5}, so
     // warps 0-3 can read bin j's TMEM lane quarters (tcgen05.ld: warp w reads quarter w % 4).
     const int pj = ORDER == 1 ? (warp & 3) : ((warp >> 1) & 1);
     const int role = ORDER == 1 ? (warp >> 2) : ((warp & 1) + 2 * (warp >> 2));
-    float *mystg = stg + pj * T::ROWS * T::SS;
+
 
     // Each bin slot pj (its 2 | 4 warps) runs independently: its own bins (group grp, slot pj),
     // chunk double buffer parity, mbarriers, named barrier (id 1 + pj) and MMA issue into its own
@@ -424,12 +402,12 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
             // ---- prep + TF32 tiles of this warp's row share (compile-time row range per role)
             {
                 const bool live = T::CH * c + lane < nb;
-                const uint32_t op_s = smem_u32(op), stg_s = smem_u32(mystg);
+                const uint32_t op_s = smem_u32(op);
                 switch (role) {
-                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
-                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
-                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
-                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, stg_s, op_s, pj, lane, fws, fsig); break;
+                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
+                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
+                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
+                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -438,15 +416,15 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 tc_fence_after();
                 const int nks = (min(T::CH, nb - T::CH * c) + 7) / 8;
                 for (int ks = 0; ks < nks; ++ks) {
-                    const unsigned char *Ah = op + ks * (T::A_STEP + T::B_STEP);
-                    const unsigned char *Bh = Ah + T::A_STEP + T::NB * pj * 32;
+                    const unsigned char *Ah = op + ks * 32;                                 // K-step: +32 B
+                    const unsigned char *Bh = op + T::A_BYTES + T::NB * pj * 128 + ks * 32;  // slot's N rows
                     const int acc0 = (c > 0 || ks > 0) ? 1 : 0;
                     const uint32_t d = tmem + T::NB * pj;
-                    umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bh, 128, 256), IDESC_J, acc0);
+                    umma_tf32(d, umma_desc_sw128(Ah), umma_desc_sw128(Bh), IDESC_J, acc0);
                     if (X3) {
                         const unsigned char *Al = Ah + T::PART_BYTES, *Bl = Bh + T::PART_BYTES;
-                        umma_tf32(d, umma_desc(Ah, 128, 256), umma_desc(Bl, 128, 256), IDESC_J, 1);
-                        umma_tf32(d, umma_desc(Al, 128, 256), umma_desc(Bh, 128, 256), IDESC_J, 1);
+                        umma_tf32(d, umma_desc_sw128(Ah), umma_desc_sw128(Bl), IDESC_J, 1);
+                        umma_tf32(d, umma_desc_sw128(Al), umma_desc_sw128(Bh), IDESC_J, 1);
                     }
                 }
                 umma_commit(&bar_buf[buf]);
@@ -480,7 +458,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
         tc_fence_after();
         if (warp < 4) {  // lane quarter = warp: this slot's Z rows
             const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
-            float *ep = epi + pj * T::ROWS * T::SS;
+            float *ep = epi + pj * T::NX * T::NZ;
             const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
 #pragma unroll
             for (int x0 = 0; x0 < T::NX; x0 += 16) {
@@ -499,7 +477,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
         asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
         // ---- deposit: FP32 REDs in global address order, the bin's entries split over its warps
         if (nbk > 0) {
-            const float *ep = epi + pj * T::ROWS * T::SS;
+            const float *ep = epi + pj * T::NX * T::NZ;
             if (ORDER == 1) {
                 for (int i = 32 * role; i < T::NDEP; i += 32 * T::WPB) {
                     const bool ok = i + lane < T::NDEP;
@@ -535,8 +513,7 @@ __global__ void __launch_bounds__(256, 3) k_asm_tf32(Geo g, const double *__rest
                 }
             }
         }
-        // the slot's staging (= epi) and rowp are rewritten by the next bin
-        asm volatile("bar.sync %0, %1;" ::"r"(1 + pj), "r"(pthreads) : "memory");
+        // (epi / rowp of this slot are rewritten only after the next bin's chunk barriers)
     }
     tc_fence_before();
     __syncthreads();
