@@ -235,18 +235,13 @@ struct PP {
 // (k & 3) 4.  For a fixed row the 32 lanes hit 32 distinct banks (no staging round trip).
 template <int ORDER, int NC, bool X3, int ROLE>
 __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t op_s, int pj,
-                                          int lane, float fws, float fsig)
+                                          const uint32_t (&lo8)[8], float fws, float fsig)
 {
     using T = PP<ORDER, NC, X3>;
     if constexpr (ROLE >= T::WPB) {
         return;
     } else {
     constexpr int R0 = ROLE * T::ROWS / T::WPB, R1 = (ROLE + 1) * T::ROWS / T::WPB;
-    // lane part of the swizzled offset for each value of (row & 7)
-    uint32_t lo8[8];
-#pragma unroll
-    for (int r7 = 0; r7 < 8; ++r7)
-        lo8[r7] = (uint32_t)((((lane >> 2) ^ r7) << 4) + (lane & 3) * 4 + r7 * 128);
     float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
     if (live) {
         if (R0 < T::NX) {
@@ -359,6 +354,11 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
     // slots' rows (possibly while they are rewritten), which only produce D lanes outside its
     // quarter(s), never read.
     const int pthreads = 32 * T::WPB;
+    // lane part of the swizzled tile offset for each value of (row & 7) (see prep_tile)
+    uint32_t lo8[8];
+#pragma unroll
+    for (int r7 = 0; r7 < 8; ++r7)
+        lo8[r7] = (uint32_t)((((lane >> 2) ^ r7) << 4) + (lane & 3) * 4 + r7 * 128);
     const bool issuer = role == 0 && lane == 0;
     uint64_t *bar_buf = bar + 2 * pj, *bar_acc = bar + 2 * T::BPC + pj;
     constexpr uint32_t IDESC_J = idesc_tf32(T::NB);
@@ -404,10 +404,10 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
                 const bool live = T::CH * c + lane < nb;
                 const uint32_t op_s = smem_u32(op);
                 switch (role) {
-                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
-                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
-                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
-                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op_s, pj, lane, fws, fsig); break;
+                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
+                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
+                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
+                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
