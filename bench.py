@@ -489,6 +489,11 @@ def main():
                                          "hbm_achieved_gbs": r["np"] * (64 + (27 if order == 1 else 125) * 9 * 4 /
                                                                         synth.ppc_of(r["cfg"])) /
                                          (r["assemble_ms"] / 1e3) / 1e9}
+                # HBM-bound variant: 64-B record read + FP32 output per particle
+                tf[f"{name}_{pname}"]["roofline"] = {
+                    "bound": "hbm", "achieved": tf[f"{name}_{pname}"]["hbm_achieved_gbs"],
+                    "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                    "frac": tf[f"{name}_{pname}"]["hbm_achieved_gbs"] / peaks.get("hbm_gbs", 6535.1)}
                 del r
         line["tf32"] = tf
 
