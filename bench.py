@@ -686,10 +686,12 @@ def main():
             tt = T.tensor([ems], device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ems = float(tt.item())
+        # the last step's matrix as read back on the host equals the device result (pipeline check)
+        e2e_ok = bool(T.equal(host_out, outs[(ke - 1) % 2].cpu()))
         h2d_bytes = sum(v.numel() * v.element_size() for v in hp.values())
         line["e2e"] = {"value": r1["np"] * world * ke / (ems / 1e3) / 1e6, "unit": UNIT,
                        "h2d_bytes_per_step": h2d_bytes,
-                       "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke,
+                       "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke, "host_copy_matches_device": e2e_ok,
                        "note": "pinned host pos/q/B -> device, sort + assemble, full mass matrix -> pinned host; "
                                "pipelined across steps (H2D of k+1 and D2H of k-1 overlap step k)"}
         # the same end-to-end pipeline with the production storage of PAPER.md:576 (FP32 positions
