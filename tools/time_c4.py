@@ -1,5 +1,5 @@
 """c4 (128^3 clustered, scalar) sort / assembly timing per order (diagnostics).
-    python tools/time_c4.py [order] [reps]"""
+    python tools/time_c4.py [order] [reps] [lib.so]"""
 import sys
 
 import torch
@@ -8,6 +8,9 @@ sys.path.insert(0, ".")
 import synth  # noqa: E402
 import paper_2604_19286_b200 as mm  # noqa: E402
 
+if len(sys.argv) > 3:
+    from paper_2604_19286_b200 import _build
+    _build.LIB = sys.argv[3]
 order = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 cfg = synth.config("c4o1")

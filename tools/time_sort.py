@@ -12,9 +12,6 @@ import paper_2604_19286_b200 as mm  # noqa: E402
 if len(sys.argv) > 3:
     from paper_2604_19286_b200 import _build
     _build.LIB = sys.argv[3]
-if len(sys.argv) > 3:
-    from paper_2604_19286_b200 import _build
-    _build.LIB = sys.argv[3]
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
 cfg = synth.config(name)
