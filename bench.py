@@ -81,14 +81,19 @@ class ClockSampler:
         self.index = index
         self.lines = []
         self.proc = None
+        self.first = threading.Event()
 
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes a while to start: the timed region begins once it reports, so
+            # that the samples fall inside the region
+            self.first.wait(timeout=10.0)
+            self.lines.clear()
         except Exception:
             self.proc = None
         return self
@@ -96,6 +101,7 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+            self.first.set()
 
     def __exit__(self, *a):
         if self.proc:
