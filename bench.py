@@ -53,6 +53,8 @@ def flops_per_particle(order, ncomp, kind="unique"):
     if kind == "pair":
         return 2 * (9 * 27 if order == 1 else 36 * 54) * ncomp // 9
     if kind == "executed":
+        if ncomp == 1:  # scalar kernels k_asm_pps: 2 | 5 DMMA per batch of 4
+            return (2 if order == 1 else 5) * 512 // 4
         return (8 if order == 1 else 35) * 512 // 4
     raise ValueError(kind)
 
