@@ -162,7 +162,9 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  *   h          sorted handle (mm_sort_by_cell) for the same grid
  *   kind       MM_SCALAR | MM_TENSOR (MM_TENSOR needs a handle sorted with B)
  *   prec       MM_FP64 (DMMA, FP64 out) | MM_TF32 | MM_TF32X3 (tcgen05 kind::tf32,
- *              FP32 out; the TF32 variant "reported separately")
+ *              FP32 out; the TF32 variant "reported separately").
+ *              The TF32 paths take whole-domain grids only (x_begin = 0, x_end = n[0]);
+ *              a slab grid returns MM_ERR_INCOMPATIBLE.
  *   sp         host, species constants (qom, dt, c > 0, sigma)
  *   accumulate 0: out = M (the owned rows are overwritten);
  *              1: out += M (species sum)
