@@ -242,7 +242,15 @@ __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, 
         return;
     } else {
     constexpr int R0 = ROLE * T::ROWS / T::WPB, R1 = (ROLE + 1) * T::ROWS / T::WPB;
+    static_assert(T::NB % 8 == 0 && T::MB % 8 == 0, "a bin's tile rows start on a swizzle period");
     float qx[T::NU], qy[T::NU], qz[T::NU], sc[NC];
+    // a lane past the bin's end prepares zeros: zero inputs give exact +0 products
+#pragma unroll
+    for (int i = 0; i < T::NU; ++i)
+        qx[i] = qy[i] = qz[i] = 0.0f;
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+        sc[c] = 0.0f;
     if (live) {
         if (R0 < T::NX) {
             pair_products<ORDER>(ca.x, qx);
@@ -253,18 +261,27 @@ __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, 
             coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
         }
     }
+    // tile row m = NB pj + r (X) | MB pj + r - NX (Z): m & 7 is a compile-time constant, so the
+    // rows are visited grouped by their swizzle phase and each lane offset lo8[m & 7] is used
+    // from one register at a time; m >> 3 splits into a per-slot base plus a constant
+    const uint32_t base_x = op_s + T::A_BYTES + (uint32_t)(T::NB / 8 * pj) * 1024;
+    const uint32_t base_z = op_s + (uint32_t)(T::MB / 8 * pj) * 1024;
 #pragma unroll
-    for (int r = R0; r < R1; ++r) {
-        float v = 0.0f;
-        if (live)
-            v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-        const int m = r < T::NX ? T::NB * pj + r : T::MB * pj + r - T::NX;   // tile row
-        const uint32_t d = op_s + (r < T::NX ? T::A_BYTES : 0) + (uint32_t)(m >> 3) * 1024 + lo8[m & 7];
-        const uint32_t hi = tf32_rna(v);
-        asm volatile("st.shared.b32 [%0], %1;" ::"r"(d), "r"(hi) : "memory");
-        if (X3)
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(d + T::PART_BYTES), "r"(tf32_rna(v - __uint_as_float(hi)))
-                         : "memory");
+    for (int r7 = 0; r7 < 8; ++r7) {
+        const uint32_t lo = lo8[r7];
+#pragma unroll
+        for (int r = R0; r < R1; ++r) {
+            const int mr = r < T::NX ? r : r - T::NX;  // row inside the bin's X or Z block
+            if ((mr & 7) != r7)
+                continue;
+            const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
+            const uint32_t d = (r < T::NX ? base_x : base_z) + (uint32_t)(mr >> 3) * 1024 + lo;
+            const uint32_t hi = tf32_rna(v);
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(d), "r"(hi) : "memory");
+            if (X3)
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(d + T::PART_BYTES), "r"(tf32_rna(v - __uint_as_float(hi)))
+                             : "memory");
+        }
     }
     }
 }
