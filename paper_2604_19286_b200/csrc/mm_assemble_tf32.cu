@@ -456,14 +456,15 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
         if (nch == 0 || bin >= nbins)
             continue;
         // ---- epilogue of this slot's bin: accumulators -> epi[pj][x][z]
-        float *myrow = nullptr;  // order 1: node row of lane & 7
         {
             const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
             const int by = rem / g.n2, bz = rem - by * g.n2;
             if (ORDER == 1) {
-                const int a8 = lane & 7;
-                myrow = row_ptr_f(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
-                                  wrapi(bz + (a8 & 1), g.n2), out, ghost, T::RL);
+                if (role == 0 && lane < 8) {  // node rows a = lane of this bin, read by the deposit
+                    const int a8 = lane;
+                    rowp[pj * 32 + a8] = row_ptr_f(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
+                                                   wrapi(bz + (a8 & 1), g.n2), out, ghost, T::RL);
+                }
             } else if (role == 0 && lane < 27) {
                 const int a = lane;
                 rowp[pj * 32 + a] = row_ptr_f(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1),
@@ -497,14 +498,10 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             const float *ep = epi + pj * T::NX * T::NZ;
             if (ORDER == 1) {
                 for (int i = 32 * role; i < T::NDEP; i += 32 * T::WPB) {
-                    const bool ok = i + lane < T::NDEP;
-                    const int t = ok ? tab[i + lane] : 0;
-                    const unsigned long long rp = (unsigned long long)myrow;
-                    const unsigned lo32 = __shfl_sync(0xffffffffu, (unsigned)rp, t & 7);
-                    const unsigned hi32 = __shfl_sync(0xffffffffu, (unsigned)(rp >> 32), t & 7);
-                    float *row = (float *)(((unsigned long long)hi32 << 32) | lo32);
-                    if (ok)
-                        red_add_f32(row + ((t >> 3) & 255), ep[t >> 11]);
+                    if (i + lane < T::NDEP) {
+                        const int t = tab[i + lane];
+                        red_add_f32(rowp[pj * 32 + (t & 7)] + ((t >> 3) & 255), ep[t >> 11]);
+                    }
                 }
             } else if (T::OT) {
                 for (int i = 32 * role; i < T::NDEP2; i += 32 * T::WPB) {
