@@ -424,7 +424,7 @@ struct O1T {
     static constexpr int XS = 36;                 // row stride (doubles): 2 wavefronts per batch LDS
     static constexpr int ROWS = 36;               // 9 X rows + 27 Z rows
     static constexpr int WARP_DOUBLES = ROWS * XS;  // 1296 (stage of 243 aliases it)
-    static constexpr size_t SMEM = (size_t)WARPS * WARP_DOUBLES * 8 + 576 * 4;
+    static constexpr size_t SMEM = (size_t)WARPS * WARP_DOUBLES * 8 + 576 * 4 + WARPS * 8 * 8;  // + node rows
 };
 
 __global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double *__restrict__ rec,
@@ -438,6 +438,7 @@ __global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double
     double *xz = dsm_o1t + warp * L::WARP_DOUBLES;
     double *stage = xz;  // [9][27] after the last batch of a bin
     int32_t *s_dep = reinterpret_cast<int32_t *>(dsm_o1t + L::WARPS * L::WARP_DOUBLES);
+    double **s_row = reinterpret_cast<double **>(s_dep + 576) + warp * 8;  // this warp's bin: node rows
     const int plane = g.n1 * g.n2;
 
     // deposit table, element e = (a, b, c) in address order of node a's row:
@@ -569,15 +570,15 @@ __global__ void __launch_bounds__(O1T::WARPS * 32) k_asm_o1t(Geo g, const double
                     }
             const int bx = bin / plane, rem = bin - bx * plane;
             const int by = rem / g.n2, bz = rem - by * g.n2;
-            const int a8 = lane & 7;
-            double *myrow = row_ptr(g, g.x_begin + bx + (a8 >> 2), wrapi(by + ((a8 >> 1) & 1), g.n1),
-                                    wrapi(bz + (a8 & 1), g.n2), out, ghost, 27 * 9);
+            if (lane < 8)
+                s_row[lane] = row_ptr(g, g.x_begin + bx + (lane >> 2), wrapi(by + ((lane >> 1) & 1), g.n1),
+                                      wrapi(bz + (lane & 1), g.n2), out, ghost, 27 * 9);
             __syncwarp();
 #pragma unroll
             for (int i = 0; i < 18; ++i) {
                 const int t = s_dep[i * 32 + lane];
                 const double v = stage[t >> 11];
-                double *row = shfl_ptr(myrow, t & 7);
+                double *row = s_row[t & 7];
                 red_add(row + ((t >> 3) & 255), v);  // unconditional (+0 contributions are harmless)
             }
         } else if (bin + nw < nbins && nb0 + lane < nb1) {
