@@ -423,3 +423,31 @@ def test_apply_constant_field_is_moment():
     s = np.stack([d["q"][p] * oracle.alpha(d["B"][p] / 2) for p in range(len(d["q"]))])  # [np,3,3]
     ref = W @ s.sum(axis=2)
     assert np.abs(y - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_keys_on_a_slab_hand_derived():
+    # Reading R12 on a slab: bx = c_x + b_x - x_begin + order - 1 (unwrapped, local),
+    # by/bz wrapped; key = (bx n1 + by) n2 + bz.  Keys worked out by hand for grid (10, 5, 6),
+    # slab [3, 7):
+    #   (3.25, 1.5, 5.75): cell (3,1,5), xi (.25,.5,.75); CIC bx 0 -> key 11;
+    #                      TSC base (-1, 0, 0) (xi_y = 1/2 ties to base 0, R4) -> bx 0 -> 11
+    #   (6.9, 4.2, 0.1):   cell (6,4,0); CIC bx 3 -> (3*5+4)*6+0 = 114;
+    #                      TSC base (0,-1,-1) -> bx 4, by 3, bz 5 -> (4*5+3)*6+5 = 143
+    #   (3.0, 0.0, 0.0):   cell (3,0,0), xi 0; CIC key 0; TSC base -1: bx 0, by 4, bz 5 -> 29
+    n, xb, xe = (10, 5, 6), 3, 7
+    pos = np.array([[3.25, 1.5, 5.75], [6.9, 4.2, 0.1], [3.0, 0.0, 0.0]])
+    q = np.ones(3)
+    assert oracle.keys(n, 1, pos, q, x_begin=xb, x_end=xe).tolist() == [11, 114, 0]
+    assert oracle.keys(n, 2, pos, q, x_begin=xb, x_end=xe).tolist() == [11, 143, 29]
+    assert oracle.nbins(n, 1, xb, xe) == 4 * 5 * 6
+    assert oracle.nbins(n, 2, xb, xe) == 5 * 5 * 6
+    # outside the slab along x: a domain error (never clamped), also for the plane below x_begin
+    for x in (2.99, 7.0, 9.5):
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.keys(n, 1, [[x, 1.0, 1.0]], [1.0], x_begin=xb, x_end=xe)
+        assert e.value.code == oracle.OR_ERR_DOMAIN
+    # the slab sort places these three exactly as the hand keys say (K = 4 padding)
+    r = oracle.sort(n, 2, 4, pos, q, x_begin=xb, x_end=xe)
+    assert r["seg_count"][[11, 29, 143]].tolist() == [1, 1, 1] and r["seg_count"].sum() == 3
+    assert r["seg_begin"][12] == 4 and r["seg_begin"][30] == 8 and r["seg_begin"][144] == 12
+    assert r["perm"].tolist() == [0, -1, -1, -1, 2, -1, -1, -1, 1, -1, -1, -1]
