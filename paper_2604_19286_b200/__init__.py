@@ -162,7 +162,9 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
         raise MMError(MM_ERR_INVALID_ARG, "pos must be [np, 3]")
     if B is not None and tuple(B.shape) != (np_, 3):
         raise MMError(MM_ERR_INVALID_ARG, "B must be [np, 3]")
-    hp = ctypes.c_void_p(handle.ptr.value if handle is not None and handle.ptr else None)
+    if handle is not None and (handle.ptr is None or not handle.ptr.value):
+        raise MMError(MM_ERR_INVALID_ARG, "handle was freed")
+    hp = ctypes.c_void_p(handle.ptr.value if handle is not None else None)
     pdt = torch.float32 if f32 else torch.float64
     fn = lib.mm_sort_by_cell_mixed if f32 else lib.mm_sort_by_cell
     st = fn(ctypes.byref(grid), int(order), int(k_pad), np_,
@@ -171,6 +173,7 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
             ctypes.byref(hp))
     _check(st)
     if handle is not None:
+        handle._ptr = hp  # the library may only grow buffers in place; keep the pointer it returned
         return handle
     return Sorted(hp, grid, order)
 

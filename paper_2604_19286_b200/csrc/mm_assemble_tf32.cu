@@ -539,14 +539,11 @@ template <int ORDER, int NC, bool X3>
 cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
 {
     using T = PP<ORDER, NC, X3>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_asm_tf32<ORDER, NC, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             T::SMEM);
-        if (e)
-            return e;
-        attr = true;
-    }
+    // per call: the attribute is per device/context (a process may drive several GPUs)
+    cudaError_t e = cudaFuncSetAttribute(k_asm_tf32<ORDER, NC, X3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         T::SMEM);
+    if (e)
+        return e;
     int dev = 0, sms = 148, smem_sm = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -773,13 +773,10 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         pt.mark("fix");
     }
     if (b.np > WARP_BIN_MAX) {
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(k_fix_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          CTA_BIN_MAX * 4)))
-                return e;
-            attr = true;
-        }
+        // per call: the attribute is per device/context (a process may drive several GPUs)
+        if ((e = cudaFuncSetAttribute(k_fix_cta, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      CTA_BIN_MAX * 4)))
+            return e;
         k_fix_cta<<<148, 1024, CTA_BIN_MAX * 4, s>>>(b.count, b.seg_begin, b.perm, b.rank, b.mid_list, b.status);
         count_launch();
     }
@@ -790,19 +787,16 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     if (b.np > 0) {
         const unsigned gs = blocks_for((b.np + 3) / 4, T);
         constexpr int SCAT_SMEM = 256 * 4 * 64;
-        static bool scat_attr = false;
-        if (!scat_attr) {
-            if ((e = cudaFuncSetAttribute(k_scatter<true, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SCAT_SMEM)) ||
-                (e = cudaFuncSetAttribute(k_scatter<false, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SCAT_SMEM)) ||
-                (e = cudaFuncSetAttribute(k_scatter<true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SCAT_SMEM)) ||
-                (e = cudaFuncSetAttribute(k_scatter<false, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          SCAT_SMEM)))
-                return e;
-            scat_attr = true;
-        }
+        // per call: the attribute is per device/context (a process may drive several GPUs)
+        if ((e = cudaFuncSetAttribute(k_scatter<true, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SCAT_SMEM)) ||
+            (e = cudaFuncSetAttribute(k_scatter<false, double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SCAT_SMEM)) ||
+            (e = cudaFuncSetAttribute(k_scatter<true, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SCAT_SMEM)) ||
+            (e = cudaFuncSetAttribute(k_scatter<false, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      SCAT_SMEM)))
+            return e;
         if (b.f32) {
             const float *pf = reinterpret_cast<const float *>(b.pos), *bf = reinterpret_cast<const float *>(b.B);
             const bool v16 = ((uintptr_t)pf % 16 == 0) && ((uintptr_t)bf % 16 == 0) && ((uintptr_t)b.q % 32 == 0);

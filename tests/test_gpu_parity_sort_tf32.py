@@ -172,3 +172,44 @@ def test_tf32_accumulate_species_sum(order, kind):
     ref = oracle.assemble(n, order, kind, d1["pos"], d1["q"], B1, qom=1.0)
     ref = oracle.assemble(n, order, kind, d2["pos"], d2["q"], B2, qom=-256.0, out=ref, accumulate=True)
     assert rel_err(out.cpu().numpy().astype(np.float64), ref) <= 2e-3
+
+
+# ------------------------------------------------ store-first deposit (order-1 tensor kernel)
+@pytest.mark.parametrize("n,xb,xe", [((8, 8, 8), 0, None), ((7, 9, 5), 0, None), ((9, 6, 7), 2, 7),
+                                     ((12, 6, 6), 3, 4), ((10, 5, 6), 0, 9)])
+@pytest.mark.parametrize("npart", [0, 7, 3000])
+def test_store_first_sparse_and_odd(n, xb, xe, npart):
+    """Output rows start as NaN: every owned and ghost row must be written by the kernel
+    (colour-0 stores, zero tasks for the rows n mod 2 leaves uncovered), with empty bins, odd
+    extents and slabs of odd width."""
+    m = mm()
+    xe_ = n[0] if xe is None else xe
+    rng = np.random.default_rng(npart + 7 * n[0])
+    lo = np.array([xb, 0, 0], dtype=np.float64)
+    ext = np.array([xe_ - xb, n[1], n[2]], dtype=np.float64)
+    pos = lo + rng.random((npart, 3)) * ext
+    pos = np.minimum(pos, np.nextafter(lo + ext, 0))
+    d = {"pos": pos, "q": rng.uniform(-1, 1, npart), "B": rng.uniform(-1, 1, (npart, 3))}
+    g = m.Grid(n, (1.0, 1.0, 1.0), xb, xe_)
+    dd = to_dev(d)
+    h = m.mm_sort_by_cell(g, 1, 4, dd["pos"], dd["q"], dd["B"])
+    out = torch.full(m.out_shape(g, 1, 9), float("nan"), dtype=torch.float64, device="cuda")
+    ghost = None
+    if m.is_slab(g):
+        ghost = torch.full(m.ghost_shape(g, 1, 9), float("nan"), dtype=torch.float64, device="cuda")
+    m.mm_assemble(h, 9, m.MM_FP64, m.Species(), out, ghost)
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert np.isfinite(o).all()
+    # the whole-domain oracle of the same particles (all inside the slab): the owned rows are its
+    # node planes [x_begin, x_end), the ghost plane is its node plane x_end (mod n0)
+    ref = oracle.assemble(n, 1, 9, d["pos"], d["q"], d["B"]).reshape(n[0], n[1] * n[2] * 27, 9)
+    assert rel_err(o.reshape(-1, 27, 9), ref[xb:xe_].reshape(-1, 27, 9)) <= 1e-12
+    if ghost is not None:
+        gh = ghost.cpu().numpy()
+        assert np.isfinite(gh).all()
+        assert rel_err(gh.reshape(-1, 27, 9), ref[xe_ % n[0]].reshape(-1, 27, 9)) <= 1e-12
+    # accumulate=1 on top of the assembled matrix doubles it (RED path, no store-first)
+    m.mm_assemble(h, 9, m.MM_FP64, m.Species(), out, ghost, accumulate=True)
+    torch.cuda.synchronize()
+    assert np.allclose(out.cpu().numpy(), 2 * o, rtol=0, atol=1e-13 * (1 + np.abs(o).max()))
