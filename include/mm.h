@@ -55,7 +55,8 @@ typedef enum {
     MM_ERR_NONFINITE = 3,     /* NaN/Inf in pos, q or B                        */
     MM_ERR_INCOMPATIBLE = 4,  /* handle/order/kind/precision mismatch          */
     MM_ERR_OUT_OF_MEMORY = 5, /* device allocation failed                      */
-    MM_ERR_CUDA = 6           /* CUDA runtime / launch error                   */
+    MM_ERR_CUDA = 6,          /* CUDA runtime / launch error                   */
+    MM_ERR_NCCL = 7           /* NCCL unavailable or a communicator call failed */
 } mm_status;
 
 typedef enum { MM_SCALAR = 1, MM_TENSOR = 9 } mm_kind; /* value = components C */
@@ -82,6 +83,7 @@ typedef struct {
 } mm_species;
 
 typedef struct mm_sorted mm_sorted; /* opaque, library-owned device storage */
+typedef struct mm_comm mm_comm;     /* opaque, library-owned NCCL communicator + comm stream */
 
 typedef struct {
     int64_t np;        /* particles sorted                                        */
@@ -163,9 +165,7 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
  *   kind       MM_SCALAR | MM_TENSOR (MM_TENSOR needs a handle sorted with B)
  *   prec       MM_FP64 (DMMA, FP64 out) | MM_TF32 | MM_TF32X3 (tcgen05 kind::tf32,
  *              FP32 out; the TF32 variant "reported separately").
- *              The TF32 paths take whole-domain grids only (x_begin = 0, x_end = n[0]);
- *              a slab grid returns MM_ERR_INCOMPATIBLE.
- *   sp         host, species constants (qom, dt, c > 0, sigma)
+ * *   sp         host, species constants (qom, dt, c > 0, sigma)
  *   accumulate 0: out = M (the owned rows are overwritten);
  *              1: out += M (species sum)
  *   out        device, [(x_end-x_begin)*n1*n2][S][C] (layout above); FP64 for
@@ -228,6 +228,62 @@ mm_status mm_slab_partition(const mm_grid *g, int64_t np, const double *pos, con
  */
 mm_status mm_ghost_add(const mm_grid *g, int order, mm_kind kind, double *out, const double *recv,
                        int first_plane, int nplanes, void *stream);
+
+/*
+ * Multi-GPU: x-slab decomposition with particles owned by cell and the ghost-plane reduction over
+ * NCCL send/recv (north_star, the "sort & communicate"
+ * stage and the task-based overlap of communication with compute).  One process per GPU.
+ *
+ * mm_comm_unique_id — ncclGetUniqueId into `uid` (host, 128 bytes).  Call on one rank and
+ *   broadcast the bytes to all ranks (e.g. over a torch.distributed process group).
+ * mm_comm_create — ncclCommInitRank(nranks, uid, rank) on the CURRENT device, plus a
+ *   non-blocking communication stream owned by the communicator.  Collective over the ranks.
+ *   Released only by mm_comm_free (which waits for the comm stream).
+ * NCCL is loaded at run time (libnccl.so.2); without it these calls return MM_ERR_NCCL.
+ */
+mm_status mm_comm_unique_id(void *uid);
+mm_status mm_comm_create(int nranks, int rank, const void *uid, mm_comm **out);
+void mm_comm_free(mm_comm *comm);
+
+/*
+ * mm_ghost_exchange — the ghost-plane reduction of one rank's slab on a periodic ring of ranks:
+ *   order 1: ghost plane 0 (node plane x_end)     -> rank r+1, added into its owned plane 0
+ *   order 2: ghost plane 0 (node plane x_begin-1) -> rank r-1, added into its last owned plane;
+ *            ghost planes 1, 2 (x_end, x_end+1)   -> rank r+1, added into its owned planes 0, 1
+ * Every rank posts send(next), recv(prev), send(prev), recv(next) in one NCCL group on the
+ * communicator's stream, which first waits for `stream`; `stream` waits for the transfer before
+ * the add kernels.  Asynchronous.  Collective: every rank of the communicator calls it.
+ *   comm    communicator of nranks ranks; rank r owns the slab `g` (slab width >= order on
+ *           every rank).  A communicator of ONE rank exchanges with itself (self ring): then `g`
+ *           must be the whole domain and the ghost planes are those of the slab [0, n0).
+ *   g, order, kind, prec  as for mm_assemble; prec selects FP64 (out/ghost double) or FP32
+ *   out     device, owned rows [(x_end-x_begin)*n1*n2][S][C] (receives the neighbours' planes)
+ *   ghost   device, this rank's ghost planes [mm_ghost_planes(order)*n1*n2][S][C] (sent; not
+ *           modified)
+ * Receive buffers are owned by the communicator; successive exchanges on one communicator must
+ * be ordered on one stream.  Errors: MM_ERR_INCOMPATIBLE for a whole grid with > 1 rank or a
+ * slab grid with 1 rank; MM_ERR_NCCL for a failed NCCL call.
+ */
+mm_status mm_ghost_exchange(mm_comm *comm, const mm_grid *g, int order, mm_kind kind, mm_precision prec, void *out,
+                            void *ghost, void *stream);
+
+/*
+ * mm_assemble_slab — mm_assemble on this rank's slab followed by the ghost reduction, with the
+ * exchange overlapped with the assembly: the bin planes whose support windows
+ * reach a ghost plane (order 1: the last bin plane; order 2: the first and the last two) are
+ * assembled first into `ghost`, the ghost planes travel on the communicator's stream while the
+ * interior bins are assembled on `stream`, then the received planes are added into `out`.  On
+ * return (stream order) `out` holds the complete owned rows of the global mass matrix.
+ *   h, kind, prec, sp   as for mm_assemble (h sorted for this rank's slab grid; with a one-rank
+ *                       communicator, for the whole grid: the self ring)
+ *   accumulate          0: out = M; 1: out += M (species sum)
+ *   out                 device, owned rows (layout of mm_assemble)
+ *   ghost               device scratch [mm_ghost_planes(order)*n1*n2][S][C]; zeroed by the call
+ *   comm, stream        communicator of this rank; cudaStream_t as void*
+ * Asynchronous; collective over the communicator.  Errors as mm_assemble and mm_ghost_exchange.
+ */
+mm_status mm_assemble_slab(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, int accumulate,
+                           void *out, void *ghost, mm_comm *comm, void *stream);
 
 /* Number of ghost node planes of a slab: 1 (order 1) or 3 (order 2). */
 int mm_ghost_planes(int order);

@@ -11,6 +11,9 @@ Entry points (same names as the C ABI):
     mm_sorted_view(handle) -> dict of device tensors (perm, seg_begin, seg_count, rec)
     mm_assemble(handle, kind, prec, species, out, ghost=None, accumulate=False)
     mm_ghost_add(grid, order, kind, out, recv, first_plane, nplanes)
+    mm_comm_unique_id() / mm_comm_create(nranks, rank, uid) -> Comm / mm_comm_free(comm)
+    mm_ghost_exchange(comm, grid, order, kind, prec, out, ghost)
+    mm_assemble_slab(handle, kind, prec, species, out, ghost, comm, accumulate=False)
     mm_free(handle)
 plus helpers (Grid, Species, out_shape, ghost_shape, ...).
 """
@@ -24,16 +27,18 @@ import torch
 from . import _build
 
 MM_OK, MM_ERR_INVALID_ARG, MM_ERR_DOMAIN, MM_ERR_NONFINITE, MM_ERR_INCOMPATIBLE, MM_ERR_OUT_OF_MEMORY, \
-    MM_ERR_CUDA = range(7)
+    MM_ERR_CUDA, MM_ERR_NCCL = range(8)
 MM_SCALAR, MM_TENSOR = 1, 9
 MM_FP64, MM_TF32, MM_TF32X3 = 0, 1, 2
 
 _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM_ERR_NONFINITE",
-                 4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA"}
+                 4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA", 7: "MM_ERR_NCCL"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_slab_partition", "mm_sorted_view", "mm_assemble", "mm_apply", "mm_ghost_add", "mm_ghost_planes",
-           "mm_out_elems", "mm_free", "mm_last_error", "mm_version", "mm_launch_count"]
+EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
+           "mm_assemble_slab", "mm_apply", "mm_ghost_add", "mm_ghost_exchange", "mm_ghost_planes", "mm_out_elems",
+           "mm_comm_unique_id", "mm_comm_create", "mm_comm_free", "mm_free", "mm_last_error", "mm_version",
+           "mm_launch_count"]
 
 
 class MMError(RuntimeError):
@@ -91,6 +96,16 @@ def load_library(build_if_missing: bool = True):
     lib.mm_ghost_planes.restype = I
     lib.mm_out_elems.argtypes = [P, I, I]
     lib.mm_out_elems.restype = I64
+    lib.mm_assemble_slab.argtypes = [P, I, I, P, I, P, P, P, P]
+    lib.mm_assemble_slab.restype = I
+    lib.mm_ghost_exchange.argtypes = [P, P, I, I, I, P, P, P]
+    lib.mm_ghost_exchange.restype = I
+    lib.mm_comm_unique_id.argtypes = [P]
+    lib.mm_comm_unique_id.restype = I
+    lib.mm_comm_create.argtypes = [I, I, P, P]
+    lib.mm_comm_create.restype = I
+    lib.mm_comm_free.argtypes = [P]
+    lib.mm_comm_free.restype = None
     lib.mm_free.argtypes = [P]
     lib.mm_free.restype = None
     lib.mm_last_error.restype = ctypes.c_char_p
@@ -286,3 +301,75 @@ def assemble(grid: mm_grid, order: int, kind: int, pos, q, B=None, species: mm_s
         ghost = torch.empty(ghost_shape(grid, order, kind), dtype=torch.float64, device=pos.device)
     mm_assemble(h, kind, MM_FP64, species, out, ghost, stream=stream)
     return (out, h) if ghost is None else (out, h, ghost)
+
+
+# ----------------------------------------------------------------- multi-GPU (include/mm.h)
+class Comm:
+    """Owner of an ``mm_comm*`` (NCCL communicator + comm stream), released by mm_comm_free."""
+
+    def __init__(self, ptr, nranks: int, rank: int):
+        self._ptr = ptr
+        self.nranks = nranks
+        self.rank = rank
+
+    @property
+    def ptr(self):
+        return self._ptr
+
+    def __del__(self):
+        try:
+            mm_comm_free(self)
+        except Exception:
+            pass
+
+
+def mm_comm_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes): call on one rank, broadcast to the others."""
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().mm_comm_unique_id(buf))
+    return buf.raw
+
+
+def mm_comm_create(nranks: int, rank: int, uid: bytes) -> Comm:
+    """ncclCommInitRank on the current CUDA device (collective over the ranks)."""
+    if len(uid) != 128:
+        raise MMError(MM_ERR_INVALID_ARG, "uid must be 128 bytes")
+    p = ctypes.c_void_p()
+    _check(load_library().mm_comm_create(int(nranks), int(rank), ctypes.create_string_buffer(uid, 128),
+                                         ctypes.byref(p)))
+    return Comm(p, nranks, rank)
+
+
+def mm_comm_free(comm: Comm):
+    if comm is not None and comm._ptr is not None and comm._ptr.value:
+        load_library().mm_comm_free(comm._ptr)
+        comm._ptr = None
+
+
+def comm_from_group(group=None) -> Comm:
+    """Bootstrap an mm_comm over a torch.distributed process group: rank 0 draws the NCCL unique
+    id, broadcast_object_list sends it to every rank, each rank calls mm_comm_create."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [mm_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return mm_comm_create(world, rank, obj[0])
+
+
+def mm_ghost_exchange(comm: Comm, grid: mm_grid, order: int, kind: int, prec: int, out, ghost, stream=None):
+    """Ghost-plane reduction over NCCL inside libmm (include/mm.h)."""
+    dt = torch.float64 if int(prec) == MM_FP64 else torch.float32
+    _check(load_library().mm_ghost_exchange(comm.ptr, ctypes.byref(grid), int(order), int(kind), int(prec),
+                                            _dev_ptr(out, dt, name="out"), _dev_ptr(ghost, dt, name="ghost"),
+                                            _stream_ptr(stream)))
+
+
+def mm_assemble_slab(handle: Sorted, kind: int, prec: int, species: mm_species, out, ghost, comm: Comm,
+                     accumulate: bool = False, stream=None):
+    """Slab assembly + ghost reduction with the exchange overlapped (include/mm.h).  `ghost` is
+    scratch of ghost_shape(grid, order, kind)."""
+    dt = torch.float64 if int(prec) == MM_FP64 else torch.float32
+    _check(load_library().mm_assemble_slab(handle.ptr, int(kind), int(prec), ctypes.byref(species),
+                                           int(bool(accumulate)), _dev_ptr(out, dt, name="out"),
+                                           _dev_ptr(ghost, dt, name="ghost"), comm.ptr, _stream_ptr(stream)))
+    return out

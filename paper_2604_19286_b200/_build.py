@@ -18,8 +18,8 @@ PROBE_LIB = os.path.join(HERE, "libmm_probe.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
-         "-I", os.path.join(ROOT, "include")]
-LIB_SOURCES = ["mm_api.cu", "mm_sort.cu", "mm_assemble_fp64.cu", "mm_assemble_o1t.cu", "mm_assemble_tf32.cu", "mm_apply.cu", "mm_halo.cu"]
+         "-I", os.path.join(ROOT, "include"), "-ldl"]
+LIB_SOURCES = ["mm_api.cu", "mm_sort.cu", "mm_assemble_fp64.cu", "mm_assemble_o1t.cu", "mm_assemble_tf32.cu", "mm_apply.cu", "mm_halo.cu", "mm_comm.cu"]
 PROBE_SOURCES = ["mm_probe.cu"]
 _lock = threading.Lock()
 

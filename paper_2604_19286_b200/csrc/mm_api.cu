@@ -136,6 +136,7 @@ Geo make_geo(const mm_grid &g, int order)
     o.ih1 = 1.0 / g.h[1];
     o.ih2 = 1.0 / g.h[2];
     o.h_pow2 = pow2(g.h[0]) && pow2(g.h[1]) && pow2(g.h[2]);
+    o.bx0 = 0;
     return o;
 }
 
@@ -334,32 +335,90 @@ mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)
     return MM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+mm_status check_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, const void *out)
+{
+    if (!h || !sp || !out)
+        return fail(MM_ERR_INVALID_ARG, "NULL handle, species or out");
+    if (!h->valid)
+        return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
+    if (kind != MM_SCALAR && kind != MM_TENSOR)
+        return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
+    if (prec != MM_FP64 && prec != MM_TF32 && prec != MM_TF32X3)
+        return fail(MM_ERR_INVALID_ARG, "precision must be MM_FP64, MM_TF32 or MM_TF32X3");
+    if (kind == MM_TENSOR && !h->has_B && h->np > 0)
+        return fail(MM_ERR_INCOMPATIBLE, "MM_TENSOR needs a handle sorted with B");
+    if (!(sp->c > 0.0) || !std::isfinite(sp->qom) || !std::isfinite(sp->dt) || !std::isfinite(sp->sigma) ||
+        !std::isfinite(sp->c))
+        return fail(MM_ERR_INVALID_ARG, "species constants must be finite with c > 0");
+    return MM_OK;
+}
+
+// The assembly kernels over the bin planes [bx_lo, bx_hi) of a handle (the whole range for
+// mm_assemble; boundary / interior ranges for mm_assemble_slab).  work_idx selects the launch's
+// work counter (zeroed by the caller).
+cudaError_t enqueue_range(const mm_sorted *h, mm::Geo geo, mm_kind kind, mm_precision prec, const mm_species *sp,
+                          void *out, void *ghost, int bx_lo, int bx_hi, int work_idx, cudaStream_t s)
+{
+    const int64_t plane = (int64_t)h->g.n[1] * h->g.n[2];
+    if (bx_hi <= bx_lo)
+        return cudaSuccess;
+    geo.bx0 = bx_lo;
+    mm::AsmArgs a;
+    a.work = h->d_work + work_idx;
+    a.rec = h->rec;
+    a.rec_stride = h->has_B ? 8 : 4;
+    a.seg_begin = h->seg_begin + plane * bx_lo;
+    a.nbins = plane * (bx_hi - bx_lo);
+    a.ncomp = (int)kind;
+    a.wscale = sp->qom * sp->dt / 2.0 / sp->c;
+    a.sigma = sp->sigma;
+    a.out = static_cast<double *>(out);
+    a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
+    if (prec == MM_FP64)
+        return mm::assemble_fp64_enqueue(geo, a, s);
+    return mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);
+}
+
+int64_t row_elems(const mm_sorted *h, mm_kind kind)
+{
+    const int64_t S = (2 * h->order + 1) * (2 * h->order + 1) * (2 * h->order + 1);
+    return S * (int64_t)kind;
+}
+
+}  // namespace
+
+namespace mm {
+mm_status api_fail(mm_status st, const char *fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+}  // namespace mm
+
+extern "C" {
+
 mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, int accumulate,
                       void *out, void *ghost, void *stream)
 {
     try {
-        if (!h || !sp || !out)
-            return fail(MM_ERR_INVALID_ARG, "NULL handle, species or out");
-        if (!h->valid)
-            return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
-        if (kind != MM_SCALAR && kind != MM_TENSOR)
-            return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
-        if (prec != MM_FP64 && prec != MM_TF32 && prec != MM_TF32X3)
-            return fail(MM_ERR_INVALID_ARG, "precision must be MM_FP64, MM_TF32 or MM_TF32X3");
-        if (kind == MM_TENSOR && !h->has_B && h->np > 0)
-            return fail(MM_ERR_INCOMPATIBLE, "MM_TENSOR needs a handle sorted with B");
-        if (!(sp->c > 0.0) || !std::isfinite(sp->qom) || !std::isfinite(sp->dt) || !std::isfinite(sp->sigma) ||
-            !std::isfinite(sp->c))
-            return fail(MM_ERR_INVALID_ARG, "species constants must be finite with c > 0");
+        mm_status st = check_assemble(h, kind, prec, sp, out);
+        if (st)
+            return st;
         mm::Geo geo = mm::make_geo(h->g, h->order);
         if (!geo.periodic_x && !ghost)
             return fail(MM_ERR_INVALID_ARG, "slab grid needs a ghost buffer");
         const size_t esz = prec == MM_FP64 ? sizeof(double) : sizeof(float);
-        if (prec != MM_FP64 && !geo.periodic_x)
-            return fail(MM_ERR_INCOMPATIBLE, "the TF32 paths support whole-domain grids only in this version");
         cudaStream_t s = (cudaStream_t)stream;
-        const int64_t S = (2 * h->order + 1) * (2 * h->order + 1) * (2 * h->order + 1);
-        const int64_t rowlen = S * (int64_t)kind;
+        const int64_t rowlen = row_elems(h, kind);
         const int64_t nout = (int64_t)(h->g.x_end - h->g.x_begin) * h->g.n[1] * h->g.n[2] * rowlen;
         const int64_t nghost = geo.periodic_x ? 0 : (int64_t)mm_ghost_planes(h->order) * h->g.n[1] * h->g.n[2] * rowlen;
         cudaError_t e = cudaSuccess;
@@ -370,29 +429,117 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
             if (e)
                 return cuda_fail(e, "mm_assemble memset");
         }
-        e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t), s);
+        e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
         if (e)
             return cuda_fail(e, "mm_assemble memset");
-        mm::AsmArgs a;
-        a.work = h->d_work;
-        a.rec = h->rec;
-        a.rec_stride = h->has_B ? 8 : 4;
-        a.seg_begin = h->seg_begin;
-        a.nbins = h->nbins;
-        a.ncomp = (int)kind;
-        a.wscale = sp->qom * sp->dt / 2.0 / sp->c;
-        a.sigma = sp->sigma;
-        a.out = static_cast<double *>(out);
-        a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
-        if (prec == MM_FP64)
-            e = mm::assemble_fp64_enqueue(geo, a, s);
-        else
-            e = mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);
+        e = enqueue_range(h, geo, kind, prec, sp, out, ghost, 0, geo.nbx, 0, s);
         if (e)
             return cuda_fail(e, "mm_assemble launch");
         return MM_OK;
     } catch (...) {
         return fail(MM_ERR_CUDA, "unexpected exception in mm_assemble");
+    }
+}
+
+mm_status mm_ghost_exchange(mm_comm *comm, const mm_grid *g, int order, mm_kind kind, mm_precision prec, void *out,
+                            void *ghost, void *stream)
+{
+    try {
+        mm_status st = check_grid(g, order);
+        if (st)
+            return st;
+        if (!comm || !out || !ghost)
+            return fail(MM_ERR_INVALID_ARG, "NULL comm, out or ghost");
+        if (kind != MM_SCALAR && kind != MM_TENSOR)
+            return fail(MM_ERR_INVALID_ARG, "kind must be MM_SCALAR or MM_TENSOR");
+        const bool whole = g->x_begin == 0 && g->x_end == g->n[0];
+        if (whole != (mm::comm_nranks(comm) == 1))
+            return fail(MM_ERR_INCOMPATIBLE, "a slab grid needs a communicator of >= 2 ranks, a whole grid one rank");
+        const int64_t S = (2 * order + 1) * (2 * order + 1) * (2 * order + 1);
+        int rc = 0;
+        cudaError_t e = mm::ghost_exchange_enqueue(comm, order, g->x_end - g->x_begin,
+                                                   (int64_t)g->n[1] * g->n[2] * S * (int64_t)kind,
+                                                   prec == MM_FP64 ? 8 : 4, out, ghost, (cudaStream_t)stream, &rc,
+                                                   nullptr, nullptr);
+        if (rc)
+            return fail(MM_ERR_NCCL, "ghost exchange: %s", mm::nccl_error(rc));
+        if (e)
+            return cuda_fail(e, "ghost exchange");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_ghost_exchange");
+    }
+}
+
+mm_status mm_assemble_slab(const mm_sorted *h, mm_kind kind, mm_precision prec, const mm_species *sp, int accumulate,
+                           void *out, void *ghost, mm_comm *comm, void *stream)
+{
+    try {
+        mm_status st = check_assemble(h, kind, prec, sp, out);
+        if (st)
+            return st;
+        if (!comm || !ghost)
+            return fail(MM_ERR_INVALID_ARG, "NULL comm or ghost");
+        const bool whole = h->g.x_begin == 0 && h->g.x_end == h->g.n[0];
+        if (whole != (mm::comm_nranks(comm) == 1))
+            return fail(MM_ERR_INCOMPATIBLE, "a slab grid needs a communicator of >= 2 ranks, a whole grid one rank");
+        mm::Geo geo = mm::make_geo(h->g, h->order);
+        geo.periodic_x = 0;  // one rank: its own ring neighbour (self ring), same path as N ranks
+        const int o = h->order, w = h->g.x_end - h->g.x_begin, nbx = geo.nbx;
+        const size_t esz = prec == MM_FP64 ? sizeof(double) : sizeof(float);
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t rowlen = row_elems(h, kind);
+        const int64_t plane_elems = (int64_t)h->g.n[1] * h->g.n[2] * rowlen;
+        cudaError_t e = cudaMemsetAsync(ghost, 0, esz * (size_t)(mm_ghost_planes(o) * plane_elems), s);
+        if (!e && !accumulate)
+            e = cudaMemsetAsync(out, 0, esz * (size_t)(w * plane_elems), s);
+        if (!e)
+            e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
+        if (e)
+            return cuda_fail(e, "mm_assemble_slab memset");
+        // boundary bin planes (their windows reach a ghost plane) first, then the exchange on the
+        // comm stream overlapped with the interior bins, then the received planes are added
+        // order 1: boundary bx = nbx-1 (node plane x_end); order 2: bx = 0 (x_begin-1) and
+        // bx = nbx-2, nbx-1 (x_end, x_end+1)
+        int lo_hi = 0, hi_lo = nbx - 1;
+        if (o == 2) {
+            lo_hi = 1;
+            hi_lo = nbx - 2;
+            if (hi_lo < lo_hi)
+                hi_lo = lo_hi;
+        }
+        e = enqueue_range(h, geo, kind, prec, sp, out, ghost, 0, lo_hi, 0, s);
+        if (!e)
+            e = enqueue_range(h, geo, kind, prec, sp, out, ghost, hi_lo, nbx, 1, s);
+        if (e)
+            return cuda_fail(e, "mm_assemble_slab launch");
+        int rc = 0;
+        // the interior launch is enqueued between the event the comm stream waits for and the
+        // wait for the received planes: ghost_exchange_enqueue records ev_ready first
+        struct Interior {
+            const mm_sorted *h;
+            mm::Geo geo;
+            mm_kind kind;
+            mm_precision prec;
+            const mm_species *sp;
+            void *out, *ghost;
+            int lo, hi;
+            cudaStream_t s;
+        } in = {h, geo, kind, prec, sp, out, ghost, lo_hi, hi_lo, s};
+        e = mm::ghost_exchange_enqueue(
+            comm, o, w, plane_elems, (int)esz, out, ghost, s, &rc,
+            [](void *p) {
+                const Interior *q = static_cast<const Interior *>(p);
+                return enqueue_range(q->h, q->geo, q->kind, q->prec, q->sp, q->out, q->ghost, q->lo, q->hi, 2, q->s);
+            },
+            &in);
+        if (rc)
+            return fail(MM_ERR_NCCL, "ghost exchange: %s", mm::nccl_error(rc));
+        if (e)
+            return cuda_fail(e, "mm_assemble_slab");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_assemble_slab");
     }
 }
 

@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
                         stage[mr * 54 + nc] = acc[nt][v];
                 }
         }
-        const int bx = (int)(bin / plane), rem = bin - bx * plane;
+        const int bxl = (int)(bin / plane), rem = bin - bxl * plane, bx = g.bx0 + bxl;
         const int by = rem / g.n2, bz = rem - by * g.n2;
         if (threadIdx.x < 27) {
             const int a = threadIdx.x;
@@ -493,7 +493,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                     if (x < L::NX && z < L::NZ)
                         stage[x * L::NZ + z] = acc[mt][v];
                 }
-            const int bx = bin / plane, rem = bin - bx * plane;
+            const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
             const int by = rem / g.n2, bz = rem - by * g.n2;
             if (lane < L::NA) {
                 const int a = lane;

@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, O1T_MINB)
             nn0 = __ldg(seg_begin + (nbins - 1 - t - 2 * W));
             nn1 = __ldg(seg_begin + (nbins - t - 2 * W));
         }
-        const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+        const int bxl = (int)(bin / plane), rem = (int)(bin - (int64_t)bxl * plane), bx = g.bx0 + bxl;
         const int by = rem / g.n2, bz = rem - by * g.n2;
         if (b1 > b0) {
             {

@@ -457,7 +457,7 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             continue;
         // ---- epilogue of this slot's bin: accumulators -> epi[pj][x][z]
         {
-            const int bx = (int)(bin / plane), rem = (int)(bin - (int64_t)bx * plane);
+            const int bxl = (int)(bin / plane), rem = (int)(bin - (int64_t)bxl * plane), bx = g.bx0 + bxl;
             const int by = rem / g.n2, bz = rem - by * g.n2;
             if (ORDER == 1) {
                 if (role == 0 && lane < 8) {  // node rows a = lane of this bin, read by the deposit

@@ -18,6 +18,8 @@ struct Geo {
     int nbx;         // bins along axis 0 = x_end - x_begin + order - 1
     double ih0, ih1, ih2;  // 1/h, exact when the spacing is a power of two
     int h_pow2;            // all three spacings powers of two: x/h == x * (1/h) bit for bit
+    int bx0;               // assembly launches over a range of bin planes: bin 0 of the launch
+                           // is bin plane bx0 (seg_begin is offset by the caller)
 };
 
 Geo make_geo(const mm_grid &g, int order);
@@ -74,6 +76,15 @@ cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cuda
 // ---- operator apply (mm_apply.cu) -------------------------------------------
 cudaError_t apply_enqueue(const Geo &geo, int ncomp, const double *M, const double *E, double *y, int accumulate,
                           cudaStream_t s);
+
+// ---- communicator (mm_comm.cu) -----------------------------------------------
+mm_status api_fail(mm_status st, const char *fmt, ...);  // sets mm_last_error (mm_api.cu)
+const char *nccl_error(int r);
+int comm_nranks(const mm_comm *c);
+int comm_rank(const mm_comm *c);
+cudaError_t ghost_exchange_enqueue(mm_comm *c, int order, int width, int64_t plane_elems, int elem_bytes, void *out,
+                                   void *ghost, cudaStream_t s, int *nccl_rc, cudaError_t (*between)(void *),
+                                   void *between_ctx);
 
 // ---- halo (mm_halo.cu) -----------------------------------------------------
 cudaError_t ghost_add_enqueue(double *out, const double *recv, int64_t n, cudaStream_t s);

@@ -472,19 +472,6 @@ def test_apply_pipeline_full_size(name):
     assert np.abs(y.cpu().numpy() - ref).max() <= 1e-13 * scale
 
 
-def test_tf32_rejects_slab():
-    m = mm()
-    n = (8, 6, 6)
-    g = m.Grid(n, (1.0, 1.0, 1.0), 2, 5)
-    d = to_dev(synth.particles(synth.Config("t", n, 1, "tensor", 3, seed=2), 2, 5))
-    h = m.mm_sort_by_cell(g, 1, 4, d["pos"], d["q"], d["B"])
-    out = torch.zeros(m.out_shape(g, 1, 9), dtype=torch.float32, device="cuda")
-    ghost = torch.zeros(m.ghost_shape(g, 1, 9), dtype=torch.float32, device="cuda")
-    with pytest.raises(m.MMError) as e:
-        m.mm_assemble(h, 9, m.MM_TF32, m.Species(), out, ghost)
-    assert e.value.status == m.MM_ERR_INCOMPATIBLE
-
-
 def test_apply_rejects_slab():
     m = mm()
     g = m.Grid((8, 8, 8), (1.0, 1.0, 1.0), 0, 4)
