@@ -207,9 +207,12 @@ mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, c
  *   class 0: stays      (cell in [x_begin, x_end))
  *   class 1: to r - 1   (leaves through x_begin)
  *   class 2: to r + 1   (leaves through x_end)
- * The cells outside the slab are split half-and-half between the two directions (periodic),
- * so particles may move up to half the remaining domain.  Non-finite or out-of-domain
- * positions are kept in class 0 (mm_sort_by_cell reports them).
+ * The cells outside the slab are split half-and-half between the two directions (periodic):
+ * a leaver goes towards the nearer side of the ring.  A particle that moved further than the
+ * neighbouring slab is forwarded again by the neighbour (multi-hop: the caller repeats
+ * partition + exchange on the received particles until no rank has leavers, e.g.
+ * paper_2604_19286_b200.slab.migrate).  Non-finite or out-of-domain positions are kept in
+ * class 0 (mm_sort_by_cell reports them).
  *   g          host, grid with this rank's slab
  *   pos,q,B    device, FP64 [np][3], [np], [np][3] (B may be NULL)
  *   pos_out,q_out,B_out  device, same shapes: [class 0 | class 1 | class 2], input order kept

@@ -8,8 +8,11 @@ the only data exchanged: they are sent to the slab neighbours (periodic ring)
 over torch.distributed (NCCL on GPUs, gloo in the CPU tests) and added into
 the owner's rows by the mm_ghost_add kernel.
 
-The bookkeeping here is pure index arithmetic on planes; the `add` callback
-defaults to the CUDA kernel (mm_ghost_add).
+The product path does the ghost reduction inside libmm (mm_assemble_slab /
+mm_ghost_exchange over an mm_comm, NCCL send/recv on the library's comm stream,
+overlapped with the interior bins).  exchange_ghosts below is the same routing
+table over torch.distributed: the CPU (gloo) tests check the multi-rank routing
+with it, which one GPU cannot do with NCCL.
 """
 from __future__ import annotations
 
@@ -42,9 +45,11 @@ def exchange_ghosts(out: torch.Tensor, ghost: torch.Tensor, order: int, plane_el
     out    [width * plane_elems] owned rows of this rank (any shape, contiguous)
     ghost  [nghost * plane_elems] ghost planes of this rank
     widths slab width of every rank (for the -1 direction's target plane)
-    add    add(k, src): add one received plane `src` into owned plane k (relative to x_begin).
-           The product path passes the mm_ghost_add kernel; the CPU tests a torch add.
+    add    add(k, src): add one received plane `src` into owned plane k (relative to x_begin),
+           e.g. the mm_ghost_add kernel or a torch add (required).
     """
+    if add is None:
+        raise ValueError("exchange_ghosts needs an add(k, src) callback")
     g = ghost.reshape(-1, plane_elems)
     nxt, prv = (rank + 1) % world, (rank - 1) % world
     send_next = [k for k, d, _ in ghost_routes(order, widths[rank]) if d == +1]
@@ -68,52 +73,74 @@ def exchange_ghosts(out: torch.Tensor, ghost: torch.Tensor, order: int, plane_el
     return out
 
 
-def migrate(pos: torch.Tensor, q: torch.Tensor, B, rank: int, world: int, partition, group=None):
-    """Send the particles that left this rank's slab to the slab neighbours (periodic ring) and
-    return this rank's new (pos, q, B): [stayed | received from r-1 | received from r+1].
+def migrate(pos: torch.Tensor, q: torch.Tensor, B, rank: int, world: int, partition, group=None,
+            max_rounds: int | None = None):
+    """Send the particles that left this rank's slab towards their owners and return this rank's
+    new (pos, q, B): the particles that stayed, then those received, in a deterministic order.
 
     The "sort & communicate" stage of the PIC cycle: after
     the mover, particles are owned by cell again before mm_sort_by_cell.
     partition(pos, q, B) -> (pos_o, q_o, B_o, (n_stay, n_prev, n_next)): the stable 3-way
-    partition (mm_slab_partition on GPUs; a torch stand-in in the CPU tests).
-    Messages per step: the two leaver counts, then the packed leavers [n, 7] (or [n, 4] without
-    B) to each neighbour, posted in the same order as exchange_ghosts (next first)."""
-    pos_o, q_o, B_o, (ns, npv, nnx) = partition(pos, q, B)
+    partition (mm_slab_partition on GPUs; a torch stand-in in the CPU tests) sends a particle
+    outside the slab towards the nearer side of the periodic ring.
+
+    Multi-hop: a particle that moved further than the neighbouring slab is forwarded again in
+    the next round; rounds repeat until the all-reduced number of leavers is 0 (at most about
+    world / 2 + 1 rounds, each one hop).  Per round: the two leaver counts, then the packed
+    leavers [n, 7] (or [n, 4] without B) to each neighbour, posted next-first."""
     if world == 1:
+        pos_o, q_o, B_o, _ = partition(pos, q, B)
         return pos_o, q_o, B_o
     nxt, prv = (rank + 1) % world, (rank - 1) % world
-
-    def pack(a, b):
-        cols = [pos_o[a:b], q_o[a:b, None]] + ([B_o[a:b]] if B_o is not None else [])
-        return torch.cat(cols, dim=1).contiguous()
-
-    to_prev, to_next = pack(ns, ns + npv), pack(ns + npv, ns + npv + nnx)
     dev = pos.device
-    c_next = torch.tensor([nnx], dtype=torch.int64, device=dev)
-    c_prev = torch.tensor([npv], dtype=torch.int64, device=dev)
-    r_prev = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r-1 (its to_next)
-    r_next = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r+1 (its to_prev)
-    ops = [dist.P2POp(dist.isend, c_next, nxt, group), dist.P2POp(dist.irecv, r_prev, prv, group),
-           dist.P2POp(dist.isend, c_prev, prv, group), dist.P2POp(dist.irecv, r_next, nxt, group)]
-    for req in dist.batch_isend_irecv(ops):
-        req.wait()
-    ncol = to_next.shape[1]
-    from_prev = torch.empty((int(r_prev.item()), ncol), dtype=pos.dtype, device=dev)
-    from_next = torch.empty((int(r_next.item()), ncol), dtype=pos.dtype, device=dev)
-    ops = []
-    if nnx:
-        ops.append(dist.P2POp(dist.isend, to_next, nxt, group))
-    if from_prev.shape[0]:
-        ops.append(dist.P2POp(dist.irecv, from_prev, prv, group))
-    if npv:
-        ops.append(dist.P2POp(dist.isend, to_prev, prv, group))
-    if from_next.shape[0]:
-        ops.append(dist.P2POp(dist.irecv, from_next, nxt, group))
-    if ops:
+    keep_p, keep_q, keep_B = [], [], []
+    cur = (pos, q, B)
+    limit = max_rounds if max_rounds is not None else world + 1
+    for _ in range(limit + 1):
+        pos_o, q_o, B_o, (ns, npv, nnx) = partition(*cur)
+        keep_p.append(pos_o[:ns])
+        keep_q.append(q_o[:ns])
+        if B_o is not None:
+            keep_B.append(B_o[:ns])
+        total = torch.tensor([npv + nnx], dtype=torch.int64, device=dev)
+        dist.all_reduce(total, group=group)
+        if int(total.item()) == 0:
+            break
+
+        def pack(a, b):
+            cols = [pos_o[a:b], q_o[a:b, None]] + ([B_o[a:b]] if B_o is not None else [])
+            return torch.cat(cols, dim=1).contiguous()
+
+        to_prev, to_next = pack(ns, ns + npv), pack(ns + npv, ns + npv + nnx)
+        c_next = torch.tensor([nnx], dtype=torch.int64, device=dev)
+        c_prev = torch.tensor([npv], dtype=torch.int64, device=dev)
+        r_prev = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r-1 (its to_next)
+        r_next = torch.zeros(1, dtype=torch.int64, device=dev)   # count coming from r+1 (its to_prev)
+        ops = [dist.P2POp(dist.isend, c_next, nxt, group), dist.P2POp(dist.irecv, r_prev, prv, group),
+               dist.P2POp(dist.isend, c_prev, prv, group), dist.P2POp(dist.irecv, r_next, nxt, group)]
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-    got = torch.cat([from_prev, from_next], dim=0)
-    new_pos = torch.cat([pos_o[:ns], got[:, 0:3]], dim=0).contiguous()
-    new_q = torch.cat([q_o[:ns], got[:, 3]], dim=0).contiguous()
-    new_B = torch.cat([B_o[:ns], got[:, 4:7]], dim=0).contiguous() if B_o is not None else None
+        ncol = to_next.shape[1]
+        from_prev = torch.empty((int(r_prev.item()), ncol), dtype=pos.dtype, device=dev)
+        from_next = torch.empty((int(r_next.item()), ncol), dtype=pos.dtype, device=dev)
+        ops = []
+        if nnx:
+            ops.append(dist.P2POp(dist.isend, to_next, nxt, group))
+        if from_prev.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, from_prev, prv, group))
+        if npv:
+            ops.append(dist.P2POp(dist.isend, to_prev, prv, group))
+        if from_next.shape[0]:
+            ops.append(dist.P2POp(dist.irecv, from_next, nxt, group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        got = torch.cat([from_prev, from_next], dim=0)
+        cur = (got[:, 0:3].contiguous(), got[:, 3].contiguous(),
+               got[:, 4:7].contiguous() if B_o is not None else None)
+    else:
+        raise RuntimeError(f"migration did not converge in {limit} rounds")
+    new_pos = torch.cat(keep_p, dim=0).contiguous()
+    new_q = torch.cat(keep_q, dim=0).contiguous()
+    new_B = torch.cat(keep_B, dim=0).contiguous() if B is not None else None
     return new_pos, new_q, new_B

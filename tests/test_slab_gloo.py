@@ -100,17 +100,17 @@ def partition_reference(n0, h, xb, xe):
     return part
 
 
-def _migrate_worker(rank, world, port, n, q):
+def _migrate_worker(rank, world, port, n, q, reach=1.5):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg = synth.Config("t", n, 1, "tensor", 4, seed=33)
         xb, xe = slab.slab_bounds(n[0], world, rank)
         d = synth.particles(cfg, xb, xe)
-        # the mover: every particle displaced by up to 1.5 cells along x (periodic)
+        # the mover: every particle displaced by up to `reach` cells along x (periodic)
         rng = np.random.default_rng(100 + rank)
         pos = d["pos"].copy()
-        pos[:, 0] = (pos[:, 0] + rng.uniform(-1.5, 1.5, len(pos))) % n[0]
+        pos[:, 0] = (pos[:, 0] + rng.uniform(-reach, reach, len(pos))) % n[0]
         pos[:, 0] = np.where(pos[:, 0] >= n[0], 0.0, pos[:, 0])
         t = {k: torch.from_numpy(v) for k, v in (("pos", pos), ("q", d["q"]), ("B", d["B"]))}
         p2, q2, B2 = slab.migrate(t["pos"], t["q"], t["B"], rank, world, partition_reference(n[0], 1.0, xb, xe))
@@ -119,13 +119,14 @@ def _migrate_worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_slab_migration_gloo(world):
-    n = (12, 4, 5)
+@pytest.mark.parametrize("world,reach", [(2, 1.5), (3, 1.5), (4, 7.0), (5, 10.0)])
+def test_slab_migration_gloo(world, reach):
+    # reach > slab width: particles cross several slabs and are forwarded over several rounds
+    n = (12, 4, 5) if world < 4 else (20, 4, 3)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, n, q)) for r in range(world)]
+    procs = [ctx.Process(target=_migrate_worker, args=(r, world, port, n, q, reach)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
