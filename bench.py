@@ -7,10 +7,12 @@
 A step = one pass of the whole hot path over one batch of synthetic particles
 already resident in HBM: mm_sort_by_cell (locate, key, histogram, padded scan,
 stable placement, record scatter) + mm_assemble (fused W/alpha, DMMA
-contraction, node-stencil scatter) [+ ghost exchange and mm_ghost_add at N>1].
+contraction, node-stencil scatter) [at N>1: mm_assemble_slab, the ghost exchange
+over libmm's NCCL communicator overlapped with the interior bins].
 Workload at N=1: BASELINE config[1] "c2" (64^3, CIC, 64 ppc, random B, FP64
 tensor); N>1: weak scaling, one 64^3 x-slab per GPU of a (64N)x64x64 grid.
-The order-2 config c3 is measured the same way and reported under "order2".
+The order-2 config c3 is measured the same way and reported under "order2";
+the survey's weak row (32N)x256x256 (c5 at N=8, orders 1 and 2) under "weak_c5".
 
 `--impl reference` times the oracle (plain FP64 CPU loop, oracle/) on the host
 cores on a bounded sample of the same workload.
@@ -43,8 +45,8 @@ def flops_per_particle(order, ncomp, kind="unique"):
              floor): the `roofline` figure
     plan     F_method = 2 x (MMA entries per component of the paper's tile plan: 64 | 640) x C
     pair     this build's pair-product contraction: 2 x (9 x 27 | 36 x 54) (tensor)
-    executed DMMA FLOPs issued by the pair-product kernels incl. tile padding: 8 | 35 DMMA.8x8x4
-             per batch of 4 particles"""
+    executed DMMA FLOPs issued by the pair-product kernels incl. tile padding: 5 | 35 DMMA.8x8x4
+             per batch of 4 particles (tensor; the order-1 kernel adds 3 SIMT FMAs per particle)"""
     n = 8 if order == 1 else 27
     if kind == "unique":
         return 2 * (n * (n + 1) // 2) * ncomp
@@ -55,7 +57,7 @@ def flops_per_particle(order, ncomp, kind="unique"):
     if kind == "executed":
         if ncomp == 1:  # scalar kernels k_asm_pps: 2 | 5 DMMA per batch of 4
             return (2 if order == 1 else 5) * 512 // 4
-        return (8 if order == 1 else 35) * 512 // 4
+        return (5 if order == 1 else 35) * 512 // 4
     raise ValueError(kind)
 
 
@@ -73,94 +75,144 @@ def load_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clock and throttle reasons sampled DURING the timed region: an NVML polling thread
+    (every 2 ms, so that even a region of a few tens of ms gets samples), nvidia-smi -lms 50 as
+    the fallback when NVML is unavailable."""
 
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    # NVML clocks-event reason bits (nvml.h): 0x8 hw_slowdown, 0x20 sw_thermal, 0x40 hw_thermal,
+    # 0x4 sw_power_cap
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap"}
 
     def __init__(self, index):
         self.index = index
-        self.lines = []
-        self.proc = None
-        self.first = threading.Event()
+        self.sm, self.reasons, self.mx = [], set(), None
+        self.stop = threading.Event()
+        self.nvml = None
+        self.smi = None
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.hnd = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.hnd, pynvml.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._poll, daemon=True)
             self.t.start()
-            # nvidia-smi takes a while to start: the timed region begins once it reports, so
-            # that the samples fall inside the region
-            self.first.wait(timeout=10.0)
-            self.lines.clear()
         except Exception:
-            self.proc = None
+            self.nvml = None
+            self._start_smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-            self.first.set()
+    def _poll(self):
+        p = self.nvml
+        while not self.stop.is_set():
+            try:
+                self.sm.append(float(p.nvmlDeviceGetClockInfo(self.hnd, p.NVML_CLOCK_SM)))
+                r = p.nvmlDeviceGetCurrentClocksEventReasons(self.hnd)
+                for bit, nm in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(nm)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def _start_smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.smi = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                         "--format=csv,noheader,nounits", "-lms", "50"],
+                                        stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            first = threading.Event()
+
+            def rd():
+                names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                for ln in self.smi.stdout:
+                    f = [x.strip() for x in ln.split(",")]
+                    first.set()
+                    if len(f) < 6 or self.stop.is_set():
+                        continue
+                    try:
+                        self.sm.append(float(f[0]))
+                        self.mx = float(f[1])
+                    except ValueError:
+                        continue
+                    for nm, v in zip(names, f[2:6]):
+                        if v.lower() == "active":
+                            self.reasons.add(nm)
+
+            threading.Thread(target=rd, daemon=True).start()
+            first.wait(timeout=10.0)  # nvidia-smi starts slowly: the region begins once it reports
+            self.sm.clear()
+        except Exception:
+            self.smi = None
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
+        self.stop.set()
+        if self.nvml is not None:
+            self.t.join(timeout=1)
+        if self.smi:
+            self.smi.terminate()
             try:
-                self.proc.wait(timeout=2)
+                self.smi.wait(timeout=2)
             except Exception:
-                self.proc.kill()
+                self.smi.kill()
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
-            if len(f) < 8:
-                continue
-            try:
-                sm.append(float(f[0]))
-                mx = float(f[1])
-            except ValueError:
-                continue
-            for nm, v in zip(names, f[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
-        if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+        src = "nvml" if self.nvml is not None else "nvidia-smi"
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": self.mx, "reasons": [], "samples": 0, "source": src}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": self.mx, "reasons": sorted(self.reasons),
+                "samples": len(self.sm), "source": src}
 
 
-def _oracle_cost(cfg, d):
+def _oracle_cost(cfg, d, omp=False):
     """(fixed seconds per call, seconds per particle) of the oracle on this workload: two short
     calls of 20k and 100k particles (the fixed part is the whole-grid output zeroing)."""
     import oracle
     kind = cfg.ncomp
     ts = []
-    for m in (20000, 100000):
+    for m in (20000, 100000) if not omp else (100000, 500000):
         m = min(m, len(d["q"]))
         t0 = time.perf_counter()
-        oracle.assemble(cfg.n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
+        _oracle_call(cfg, d, slice(0, m), omp)
         ts.append((m, time.perf_counter() - t0))
     (m1, t1), (m2, t2) = ts
-    b = max((t2 - t1) / max(m2 - m1, 1), 1e-9)
+    b = max((t2 - t1) / max(m2 - m1, 1), 1e-10)
     return max(t1 - b * m1, 0.0), b
 
 
-def oracle_rate(cfg, d, budget_s=12.0):
-    """Oracle (plain single-thread FP64 C loop) on a bounded sample (~budget_s) of the workload."""
+def _oracle_call(cfg, d, sl, omp):
+    """One oracle assembly of the particles d[sl] into the whole grid; returns the threads used."""
     import oracle
-    a, b = _oracle_cost(cfg, d)
     kind = cfg.ncomp
-    m = int(min(len(d["q"]), max(20000, (budget_s - a) / b)))
-    t0 = time.perf_counter()
-    oracle.assemble(cfg.n, cfg.order, kind, d["pos"][:m], d["q"][:m], d["B"][:m] if kind == 9 else None)
-    t = time.perf_counter() - t0
-    return {"value": m / t / 1e6, "unit": UNIT, "cores": 1, "kind": "oracle",
+    B = d["B"][sl] if kind == 9 else None
+    if omp:
+        return oracle.assemble_omp(cfg.n, cfg.order, kind, d["pos"][sl], d["q"][sl], B)[1]
+    oracle.assemble(cfg.n, cfg.order, kind, d["pos"][sl], d["q"][sl], B)
+    return 1
+
+
+def oracle_rate(cfg, d, budget_s=10.0):
+    """The oracle (plain FP64 C loop, oracle/) on a bounded sample (~budget_s each) of the workload:
+    on all host cores (or_assemble_omp, x-slab colouring) and single-threaded (or_assemble)."""
+    res = {}
+    for omp in (True, False):
+        a, b = _oracle_cost(cfg, d, omp)
+        m = int(min(len(d["q"]), max(20000, (budget_s - a) / b)))
+        t0 = time.perf_counter()
+        th = _oracle_call(cfg, d, slice(0, m), omp)
+        t = time.perf_counter() - t0
+        res[omp] = (m / t / 1e6, th, m, t)
+    v, th, m, t = res[True]
+    v1, _, m1, t1 = res[False]
+    return {"value": v, "unit": UNIT, "cores": th, "kind": "oracle",
             "sample": f"first {m} of {len(d['q'])} particles of {cfg.name} (input order) into the whole "
-                      f"{'x'.join(map(str, cfg.n))} grid, {t:.1f} s single-threaded (host has {os.cpu_count()} cores)"}
+                      f"{'x'.join(map(str, cfg.n))} grid, {t:.1f} s on {th} threads (or_assemble_omp: the oracle's "
+                      f"loop over x-slabs of one colour in parallel; host has {os.cpu_count()} cores)",
+            "single_core": {"value": v1, "unit": UNIT, "cores": 1,
+                            "sample": f"first {m1} particles, {t1:.1f} s, or_assemble"}}
 
 
 def run_reference(args):
@@ -169,18 +221,19 @@ def run_reference(args):
         return
     cfg = synth.config("c2")
     d = synth.particles(cfg)
-    import oracle
-    # bounded sample per step so that the whole --steps/--warmup run takes ~150 s of host time
-    a, b = _oracle_cost(cfg, d)
+    # bounded sample per step so that the whole --steps/--warmup run takes ~150 s of host time,
+    # the oracle on all host cores (or_assemble_omp)
+    a, b = _oracle_cost(cfg, d, omp=True)
     per_step = 150.0 / max(args.steps + args.warmup, 1)
     m = int(min(len(d["q"]) // 2, max(2000, (per_step - a) / b)))
     steps = []
+    th = 1
     for _ in range(args.warmup):
-        oracle.assemble(cfg.n, 1, 9, d["pos"][:m], d["q"][:m], d["B"][:m])
+        _oracle_call(cfg, d, slice(0, m), True)
     for k in range(args.steps):
         t0 = time.perf_counter()
-        sl = slice((k * m) % (len(d["q"]) - m), (k * m) % (len(d["q"]) - m) + m)
-        oracle.assemble(cfg.n, 1, 9, d["pos"][sl], d["q"][sl], d["B"][sl])
+        off = (k * m) % (len(d["q"]) - m)
+        th = _oracle_call(cfg, d, slice(off, off + m), True)
         steps.append(time.perf_counter() - t0)
     t = float(np.sum(steps))
     val = m * args.steps / t / 1e6
@@ -189,9 +242,10 @@ def run_reference(args):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": {"workload": "c2: 64^3 periodic grid, CIC (order 1), 64 ppc, random B, FP64 tensor mass matrix",
                        "sample_particles_per_step": m},
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": th, "kind": "oracle",
                              "sample": f"{m} particles per step of c2 (consecutive slices of the shuffled input), "
-                                       f"whole-grid output, single-threaded"},
+                                       f"whole-grid output, or_assemble_omp on {th} threads "
+                                       f"(host has {os.cpu_count()} cores)"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -208,6 +262,7 @@ def main():
     ap.add_argument("--no-tf32", action="store_true")
     ap.add_argument("--pipeline", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
+    ap.add_argument("--no-weak", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -216,7 +271,6 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_2604_19286_b200 as mm
-    from paper_2604_19286_b200 import slab
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -227,6 +281,19 @@ def main():
         dist.init_process_group("nccl", device_id=dev)
     mm.load_library(build_if_missing=False)
     peaks, peak_src = load_peaks()
+    # libmm's own NCCL communicator (ghost exchange inside mm_assemble_slab), bootstrapped over the
+    # torch process group; one rank: the self ring (used by the c5 weak-scaling row at N = 1)
+    # (NCCL prints its version banner on stdout at communicator creation: fd 1 -> fd 2 meanwhile,
+    # so that stdout carries only the JSON line)
+    sys.stdout.flush()
+    saved = os.dup(1)
+    os.dup2(2, 1)
+    try:
+        comm = mm.comm_from_group() if world > 1 else mm.mm_comm_create(1, 0, mm.mm_comm_unique_id())
+    finally:
+        sys.stdout.flush()
+        os.dup2(saved, 1)
+        os.close(saved)
 
     def barrier():
         if world > 1:
@@ -262,8 +329,6 @@ def main():
         out = torch.empty(mm.out_shape(grid, order, kind), dtype=odt, device=dev)
         ghost = torch.empty(mm.ghost_shape(grid, order, kind), dtype=odt, device=dev) \
             if mm.is_slab(grid) else None
-        plane_elems = grid.n[1] * grid.n[2] * (2 * order + 1) ** 3 * kind
-        widths = [cfg.n[0] // world] * world
         state = {"h": None}
         ev = []
 
@@ -272,13 +337,13 @@ def main():
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
-            mm.mm_assemble(state["h"], kind, prec, sp, out, ghost)
+            if world > 1:  # slab assembly with the ghost exchange overlapped, inside libmm
+                mm.mm_assemble_slab(state["h"], kind, prec, sp, out, ghost, comm)
+            else:
+                mm.mm_assemble(state["h"], kind, prec, sp, out, ghost)
             if record:
                 e1.record()
                 ev.append((e0, e1))
-            if world > 1:
-                slab.exchange_ghosts(out, ghost, order, plane_elems, rank, world, widths,
-                                     add=lambda k, src: mm.mm_ghost_add(grid, order, kind, out, src, k, 1))
 
         # Optional pipelined schedule (--pipeline, single GPU): the sort of batch k+1 runs on the
         # main stream while the assembly of batch k runs on a second stream (two handles).
@@ -358,7 +423,10 @@ def main():
             barrier()
             a0.record()
             for _ in range(max(5, args.steps // 10)):
-                mm.mm_assemble(state["h"], kind, prec, sp, out, ghost)
+                if world > 1:
+                    mm.mm_assemble_slab(state["h"], kind, prec, sp, out, ghost, comm)
+                else:
+                    mm.mm_assemble(state["h"], kind, prec, sp, out, ghost)
             a1.record()
             barrier()
             res["assemble_alone_ms"] = a0.elapsed_time(a1) / max(5, args.steps // 10)
@@ -624,6 +692,80 @@ def main():
         del d4
         torch.cuda.empty_cache()
 
+    # ---- the survey's weak-scaling row: (32N) x 256 x 256, one 32 x 256 x 256
+    #      x-slab (134.2 M particles, 64 ppc, random B) per GPU, FP64 tensor, orders 1 and 2; a step
+    #      = mm_sort_by_cell + mm_assemble_slab (boundary bins, ghost exchange over libmm's NCCL
+    #      communicator overlapped with the interior bins, ghost add).  N = 8 is config c5 (256^3).
+    #      At N = 1 the communicator is the self ring (same code path, the slab is the whole grid).
+    if not args.no_weak:
+        cache.clear()
+        torch.cuda.empty_cache()
+        weak = {}
+        per = 32
+        cfgw = synth.Config(f"weak{world}", (per * world, 256, 256), 1, "tensor", 64, seed=synth.SEED0 + 4)
+        xb, xe = rank * per, (rank + 1) * per
+        dw = synth.particles_device(cfgw, dev, with_B=True, x_begin=xb, x_end=xe)
+        npw = int(dw["q"].numel())
+        for order in (1, 2):
+            gw = mm.Grid(cfgw.n, x_begin=xb, x_end=xe)
+            outw = torch.empty(mm.out_shape(gw, order, 9), dtype=torch.float64, device=dev)
+            ghw = torch.empty(mm.ghost_shape(gw, order, 9), dtype=torch.float64, device=dev)
+            stw = {"h": None}
+
+            def sortw():
+                stw["h"] = mm.mm_sort_by_cell(gw, order, 4, dw["pos"], dw["q"], dw["B"], handle=stw["h"])
+
+            def asmw():
+                mm.mm_assemble_slab(stw["h"], 9, mm.MM_FP64, mm.Species(), outw, ghw, comm)
+
+            kw = max(3, min(10, args.steps))
+            for _ in range(3):
+                sortw()
+                asmw()
+            barrier()
+            ev_a = []
+            w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with ClockSampler(local) as clkw:
+                barrier()
+                w0.record()
+                for _ in range(kw):
+                    sortw()
+                    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a0.record()
+                    asmw()
+                    a1.record()
+                    ev_a.append((a0, a1))
+                w1.record()
+                barrier()
+            msw = w0.elapsed_time(w1) / kw
+            asm_w = float(np.mean([a.elapsed_time(b) for a, b in ev_a]))
+            if world > 1:
+                tt = torch.tensor([msw, asm_w], device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                msw, asm_w = (float(x) for x in tt.tolist())
+            Fw = flops_per_particle(order, 9)
+            aw = npw * Fw / (asm_w / 1e3) / 1e12
+            S = (2 * order + 1) ** 3
+            weak[f"order{order}"] = {
+                "value": npw * world / (msw / 1e3) / 1e6, "unit": UNIT, "ms_per_step": msw,
+                "assemble_slab_ms": asm_w, "particles_per_gpu": npw, "particles": npw * world, "steps": kw,
+                "exchanged_bytes_per_rank": (1 if order == 1 else 3) * 256 * 256 * S * 9 * 8,
+                "output_bytes_per_gpu": outw.numel() * 8, "clocks": clkw.summary(),
+                "roofline": {"bound": "tensor", "achieved": aw, "peak": fp64_peak, "unit": "TFLOP/s",
+                             "frac": aw / fp64_peak, "alg_flops_per_particle": Fw,
+                             "note": "mm_assemble_slab (zero-fill, boundary + interior bins, ghost exchange and "
+                                     "add), max over ranks"}}
+            mm.mm_free(stw["h"])
+            del outw, ghw
+            torch.cuda.empty_cache()
+        line["weak_c5"] = {"workload": f"({per * world})x256x256 grid, one {per}x256x256 x-slab per GPU, 64 ppc, "
+                                       "random B, FP64 tensor; particles drawn on the device (synth.particles_device)",
+                           "n_gpus": world, "grid": list(cfgw.n), "scaling": "weak",
+                           "exchange": "NCCL send/recv inside libmm (mm_assemble_slab), self ring at N = 1",
+                           **weak}
+        del dw
+        torch.cuda.empty_cache()
+
     # ---- end to end through the public API with host buffers (pinned), H2D + D2H in the timed region
     if not args.no_e2e:
         import torch as T
@@ -664,12 +806,10 @@ def main():
                 with T.cuda.stream(s_comp):
                     hs[b] = mm.mm_sort_by_cell(grid, 1, 4, dds[b]["pos"], dds[b]["q"], dds[b]["B"], handle=hs[b],
                                                stream=s_comp)
-                    mm.mm_assemble(hs[b], 9, mm.MM_FP64, sp, outs[b], ghosts[b], stream=s_comp)
                     if world > 1:
-                        slab.exchange_ghosts(outs[b], ghosts[b], 1, grid.n[1] * grid.n[2] * 27 * 9, rank, world,
-                                             [cfg.n[0] // world] * world,
-                                             add=lambda kk, src: mm.mm_ghost_add(grid, 1, 9, outs[b], src, kk, 1,
-                                                                                 stream=s_comp))
+                        mm.mm_assemble_slab(hs[b], 9, mm.MM_FP64, sp, outs[b], ghosts[b], comm, stream=s_comp)
+                    else:
+                        mm.mm_assemble(hs[b], 9, mm.MM_FP64, sp, outs[b], ghosts[b], stream=s_comp)
                 ev_c = T.cuda.Event()
                 ev_c.record(s_comp)
                 s_d2h.wait_event(ev_c)
@@ -729,6 +869,7 @@ def main():
         line["cpu_baseline"] = oracle_rate(cfg, r1["d"])
     if rank == 0:
         print(json.dumps(line), flush=True)
+    mm.mm_comm_free(comm)
     if world > 1:
         dist.destroy_process_group()
 

@@ -17,6 +17,7 @@ Parity status of each function:
   assemble                           — pinned (hand-derived single-particle
                                        goldens, dense W S W^T brute force,
                                        partition of unity, symmetries)
+  assemble_omp                       — timing only; equal to assemble (test)
 """
 from __future__ import annotations
 
@@ -58,7 +59,7 @@ def build(force: bool = False) -> str:
         if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
             tmp = _LIB + f".tmp{os.getpid()}"
             subprocess.check_call(["gcc", "-O2", "-std=c99", "-fPIC", "-shared", "-ffp-contract=off",
-                                   "-fno-fast-math", "-o", tmp, _SRC, "-lm"])
+                                   "-fno-fast-math", "-fopenmp", "-o", tmp, _SRC, "-lm"])
             os.replace(tmp, _LIB)
     return _LIB
 
@@ -82,6 +83,8 @@ def _load():
         lib.or_assemble.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P, P, P, P,
                                     ctypes.c_int]
         lib.or_apply.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
+        lib.or_assemble_omp.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P, P, P, P,
+                                        ctypes.c_int, P]
         _lib = lib
     return _lib
 
@@ -204,6 +207,25 @@ def assemble(n, order, ncomp, pos, q, B=None, h=(1.0, 1.0, 1.0), qom=1.0, dt=1.0
     if rc:
         raise OracleError(rc, "assemble")
     return out
+
+
+def assemble_omp(n, order, ncomp, pos, q, B=None, h=(1.0, 1.0, 1.0), qom=1.0, dt=1.0, c=1.0, sigma=1.0):
+    """or_assemble on all host cores (x-slab colouring; timing the CPU baseline only).
+    Returns (out, threads used)."""
+    g = _grid(n, h)
+    sp = _Species(qom, dt, c, sigma)
+    pos = _f64(pos, (-1, 3))
+    np_ = pos.shape[0]
+    q = _f64(q, (np_,))
+    B = _f64(B, (np_, 3))
+    S = (2 * order + 1) ** 3
+    out = np.empty((int(n[0]) * int(n[1]) * int(n[2]), S, ncomp))
+    th = ctypes.c_int(1)
+    rc = _load().or_assemble_omp(ctypes.byref(g), order, ncomp, ctypes.byref(sp), np_, _ptr(pos), _ptr(q), _ptr(B),
+                                 _ptr(out), 0, ctypes.byref(th))
+    if rc:
+        raise OracleError(rc, "assemble_omp")
+    return out, th.value
 
 
 def apply(n, order, ncomp, M, E, y=None, accumulate=False):

@@ -21,6 +21,9 @@
  */
 #include <math.h>
 #include <stdint.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdlib.h>
 #include <string.h>
 
@@ -399,5 +402,89 @@ int or_apply(const or_grid *g, int order, int ncomp, const double *M, const doub
         for (i = 0; i < nv; ++i)
             y[gi * nv + i] = accumulate ? y[gi * nv + i] + acc[i] : acc[i];
     }
+    return OR_OK;
+}
+
+/*
+ * or_assemble_omp — the same definition (eq_mass_matrix_general) computed by
+ * the same per-particle loop as or_assemble, on all host cores, for TIMING the CPU baseline
+ * (SURVEY.md §8(c) "An optional OpenMP variant for timing only", §8(d)).  The cells are split
+ * into `nslab` x-slabs of at least 3 cells; the particles of a slab (kept in input order) touch
+ * only node planes within one cell of the slab, so slabs of the same colour (even / odd index;
+ * an odd last slab gets a third colour) never write the same row and run in parallel, one
+ * colour after the other.  Deterministic for a given thread count; equal to or_assemble up to
+ * the order of the additions (bit-identical on dyadic-lattice inputs).  Whole periodic domain.
+ */
+int or_assemble_omp(const or_grid *g, int order, int ncomp, const or_species *sp, int64_t np,
+                    const double *pos, const double *q, const double *B, double *out, int accumulate,
+                    int *threads_used)
+{
+    const int n0 = g->n[0];
+    int nslab = n0 / 3 >= 4 ? (n0 / 3) & ~1 : n0 / 3, c, rc;  /* even when possible: 2 colours */
+    int64_t p, *cnt, *idx, *fill;
+    const int S = (2 * order + 1) * (2 * order + 1) * (2 * order + 1);
+    int64_t nn;
+    rc = check_grid(g, order);
+    if (rc)
+        return rc;
+    if (g->x_begin != 0 || g->x_end != n0 || (ncomp != 1 && ncomp != 9) || (ncomp == 9 && !B))
+        return OR_ERR_INVALID_ARG;
+    if (threads_used)
+        *threads_used = 1;
+    if (nslab < 2)
+        return or_assemble(g, order, ncomp, sp, np, pos, q, B, out, accumulate);
+    nn = (int64_t)n0 * g->n[1] * g->n[2];
+    if (!accumulate)
+        memset(out, 0, sizeof(double) * (size_t)(nn * S * ncomp));
+    /* stable bucketing of the particle indices by slab (slab k holds cells [k n0/nslab, ...)) */
+    cnt = (int64_t *)calloc((size_t)nslab + 1, sizeof(int64_t));
+    fill = (int64_t *)calloc((size_t)nslab + 1, sizeof(int64_t));
+    idx = (int64_t *)malloc(sizeof(int64_t) * (size_t)(np > 0 ? np : 1));
+    for (p = 0; p < np; ++p) {
+        int32_t cell[3];
+        double xi[3];
+        rc = or_locate(g, pos + 3 * p, cell, xi);
+        if (rc) {
+            free(cnt);
+            free(fill);
+            free(idx);
+            return rc;
+        }
+        cnt[(int64_t)cell[0] * nslab / n0 + 1] += 1;
+    }
+    for (c = 0; c < nslab; ++c)
+        cnt[c + 1] += cnt[c];
+    for (p = 0; p < np; ++p) {
+        int32_t cell[3];
+        double xi[3];
+        int k;
+        or_locate(g, pos + 3 * p, cell, xi);
+        k = (int)((int64_t)cell[0] * nslab / n0);
+        idx[cnt[k] + fill[k]++] = p;
+    }
+    for (c = 0; c < 3; ++c) {
+        int k;
+#pragma omp parallel for schedule(dynamic, 1)
+        for (k = 0; k < nslab; ++k) {
+            int colour = (nslab % 2 == 1 && k == nslab - 1) ? 2 : (k % 2);
+            int64_t i;
+            if (colour != c)
+                continue;
+            for (i = cnt[k]; i < cnt[k + 1]; ++i) {
+                const int64_t pp = idx[i];
+                or_assemble(g, order, ncomp, sp, 1, pos + 3 * pp, q + pp, B ? B + 3 * pp : NULL, out, 1);
+            }
+        }
+    }
+#ifdef _OPENMP
+    if (threads_used) {
+#pragma omp parallel
+#pragma omp single
+        *threads_used = omp_get_num_threads();
+    }
+#endif
+    free(cnt);
+    free(fill);
+    free(idx);
     return OR_OK;
 }

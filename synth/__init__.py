@@ -146,26 +146,28 @@ def particles(cfg: Config, x_begin: int = 0, x_end: int | None = None, shuffle=T
     return {"pos": np.ascontiguousarray(pos), "q": np.ascontiguousarray(q), "B": np.ascontiguousarray(B)}
 
 
-def particles_device(cfg: Config, device, with_B: bool = True) -> dict:
+def particles_device(cfg: Config, device, with_B: bool = True, x_begin: int = 0, x_end: int | None = None) -> dict:
     """The same recipe as particles() (cell counts, xi ~ U[0,1)^3, q ~ U[0.5,1.5], B ~ U[-1,1]^3,
     uniform random input order), drawn on the GPU with torch's Philox generator seeded by
-    cfg.seed.  Same distribution, NOT the same sample as particles(): bench.py uses it for the
-    large configs (c4: 134.7 M particles) whose host generation would take minutes; no parity
-    claim rests on it."""
+    cfg.seed (and x_begin), for the cell slab [x_begin, x_end) (default: the whole grid).  Same
+    distribution, NOT the same sample as particles(): bench.py uses it for the large configs
+    (c4: 134.7 M particles, the c5 weak-scaling slabs) whose host generation would take minutes;
+    the parity tests that use it compare against the oracle run on the same drawn particles."""
     import torch
     n0, n1, n2 = cfg.n
+    x_end = n0 if x_end is None else x_end
     if cfg.dist == "uniform":
         row_counts = np.full(n1, cfg.ppc, dtype=np.int64)
     else:
         row_counts = clustered_counts(n1, cfg.ppc)
     gen = torch.Generator(device=device)
-    gen.manual_seed(int(cfg.seed))
+    gen.manual_seed(int(cfg.seed) + 1000003 * int(x_begin))
     per_plane = int(row_counts.sum()) * n2
-    total = per_plane * n0
+    total = per_plane * (x_end - x_begin)
     cnt_yz = torch.from_numpy(np.repeat(row_counts, n2)).to(device)          # per (y, z) cell
     yz = torch.repeat_interleave(torch.arange(n1 * n2, device=device), cnt_yz)  # [per_plane]
-    ix = torch.arange(n0, device=device).repeat_interleave(per_plane)
-    iyz = yz.repeat(n0)
+    ix = torch.arange(x_begin, x_end, device=device).repeat_interleave(per_plane)
+    iyz = yz.repeat(x_end - x_begin)
     cell = torch.stack([ix, iyz // n2, iyz % n2], dim=1).to(torch.float64)
     del ix, iyz, yz
     h = torch.tensor(cfg.h, dtype=torch.float64, device=device)

@@ -37,8 +37,8 @@ def test_plan_and_executed_flops():
     # the paper's node-tile plan: 64 (CIC, 8x8 tile) | 640 (TSC, 10 upper 8x8 tiles) MMA entries
     assert bench.flops_per_particle(1, 9, "plan") == 2 * 64 * 9
     assert bench.flops_per_particle(2, 9, "plan") == 2 * 640 * 9
-    # executed: DMMA.8x8x4 = 8*8*4 FMA = 512 FLOP per 4 particles; tensor 8 | 35, scalar 2 | 5
-    for order, ncomp, ndmma in ((1, 9, 8), (2, 9, 35), (1, 1, 2), (2, 1, 5)):
+    # executed: DMMA.8x8x4 = 8*8*4 FMA = 512 FLOP per 4 particles; tensor 5 | 35, scalar 2 | 5
+    for order, ncomp, ndmma in ((1, 9, 5), (2, 9, 35), (1, 1, 2), (2, 1, 5)):
         assert bench.flops_per_particle(order, ncomp, "executed") == ndmma * 8 * 8 * 4 * 2 // 4
 
 
@@ -51,11 +51,12 @@ def test_alg_bytes():
 
 def test_clock_summary():
     c = bench.ClockSampler(0)
-    c.lines = ["1965, 1965, 700.1, 0x0, Not Active, Not Active, Not Active, Not Active",
-               "1950, 1965, 701.0, 0x4, Not Active, Not Active, Not Active, Active",
-               "garbage", "1965, 1965, 699.0, 0x0, Not Active, Not Active, Not Active, Not Active"]
+    c.sm, c.mx, c.reasons = [1965.0, 1950.0, 1965.0], 1965.0, {"sw_power_cap"}
     s = c.summary()
     assert s["samples"] == 3 and s["sm_mhz"] == 1965.0 and s["sm_max_mhz"] == 1965.0
     assert s["reasons"] == ["sw_power_cap"]
-    c.lines = []
+    c.sm = []
     assert c.summary()["samples"] == 0
+    # NVML reason bits map to the names the driver checks
+    assert set(bench.ClockSampler.REASONS.values()) == {"hw_slowdown", "hw_thermal_slowdown",
+                                                        "sw_thermal_slowdown", "sw_power_cap"}

@@ -451,3 +451,19 @@ def test_keys_on_a_slab_hand_derived():
     assert r["seg_count"][[11, 29, 143]].tolist() == [1, 1, 1] and r["seg_count"].sum() == 3
     assert r["seg_begin"][12] == 4 and r["seg_begin"][30] == 8 and r["seg_begin"][144] == 12
     assert r["perm"].tolist() == [0, -1, -1, -1, 2, -1, -1, -1, 1, -1, -1, -1]
+
+
+@pytest.mark.parametrize("order", [1, 2])
+@pytest.mark.parametrize("n", [(12, 5, 6), (9, 7, 5), (16, 5, 5)])
+def test_assemble_omp_equals_serial(order, n):
+    # the all-core timing variant of the oracle is the same sum in another order (x-slab
+    # colouring): equal within rounding, bit-identical on the dyadic lattice
+    from tests.helpers import rel_err
+    d = synth.particles(synth.Config("t", n, order, "tensor", 9, seed=5 + order))
+    a = oracle.assemble(n, order, 9, d["pos"], d["q"], d["B"])
+    b, th = oracle.assemble_omp(n, order, 9, d["pos"], d["q"], d["B"])
+    assert th >= 1 and rel_err(b, a) <= 1e-13
+    dl = synth.particles(synth.Config("t", n, order, "tensor", 9, seed=6), lattice=True)
+    a = oracle.assemble(n, order, 1, dl["pos"], dl["q"])
+    b, _ = oracle.assemble_omp(n, order, 1, dl["pos"], dl["q"])
+    assert (a == b).all()
