@@ -18,6 +18,12 @@ Parity status of each function:
                                        goldens, dense W S W^T brute force,
                                        partition of unity, symmetries)
   assemble_omp                       — timing only; equal to assemble (test)
+  moments                            — pinned (hand-derived single particle,
+                                       dense W^T Q, row sums of the pinned
+                                       scalar mass matrix, totals)
+  gather                             — pinned (dense W F, constant and linear
+                                       field reproduction, adjointness with
+                                       moments)
 """
 from __future__ import annotations
 
@@ -83,6 +89,9 @@ def _load():
         lib.or_assemble.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P, P, P, P,
                                     ctypes.c_int]
         lib.or_apply.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, P, ctypes.c_int]
+        lib.or_moments.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_int64, P, P, P, P,
+                                   ctypes.c_int]
+        lib.or_gather.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int64, P, P, P]
         lib.or_assemble_omp.argtypes = [P, ctypes.c_int, ctypes.c_int, P, ctypes.c_int64, P, P, P, P,
                                         ctypes.c_int, P]
         _lib = lib
@@ -226,6 +235,42 @@ def assemble_omp(n, order, ncomp, pos, q, B=None, h=(1.0, 1.0, 1.0), qom=1.0, dt
     if rc:
         raise OracleError(rc, "assemble_omp")
     return out, th.value
+
+
+def moments(n, order, nq, pos, q, v, sigma=1.0, h=(1.0, 1.0, 1.0), out=None, accumulate=False):
+    """Particle moments on the nodes, [nodes][nq] (nq = 4: rho, J; 10: + the second-moment
+    tensor) — PAPER.md:591 (oracle.c or_moments)."""
+    g = _grid(n, h)
+    pos = _f64(pos, (-1, 3))
+    np_ = pos.shape[0]
+    q = _f64(q, (np_,))
+    v = _f64(v, (np_, 3))
+    nn = int(n[0]) * int(n[1]) * int(n[2])
+    if out is None:
+        out = np.zeros((nn, nq))
+        accumulate = False
+    assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == nn * nq
+    rc = _load().or_moments(ctypes.byref(g), order, nq, float(sigma), np_, _ptr(pos), _ptr(q), _ptr(v), _ptr(out),
+                            int(bool(accumulate)))
+    if rc:
+        raise OracleError(rc, "moments")
+    return out
+
+
+def gather(n, order, pos, F, h=(1.0, 1.0, 1.0)):
+    """A nodal field F [nodes][ncomp] interpolated to the particles, [np][ncomp] — PAPER.md:96
+    (oracle.c or_gather)."""
+    g = _grid(n, h)
+    pos = _f64(pos, (-1, 3))
+    np_ = pos.shape[0]
+    nn = int(n[0]) * int(n[1]) * int(n[2])
+    F = _f64(F).reshape(nn, -1)
+    nc = F.shape[1]
+    Fp = np.zeros((np_, nc))
+    rc = _load().or_gather(ctypes.byref(g), order, nc, np_, _ptr(pos), _ptr(F), _ptr(Fp))
+    if rc:
+        raise OracleError(rc, "gather")
+    return Fp
 
 
 def apply(n, order, ncomp, M, E, y=None, accumulate=False):

@@ -488,3 +488,119 @@ int or_assemble_omp(const or_grid *g, int order, int ncomp, const or_species *sp
     free(idx);
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------ */
+/* NEXT-4: the same particle-to-grid machinery for moment  */
+/* deposition, and the grid-to-particle field gather that feeds alpha.      */
+/* ------------------------------------------------------------------------ */
+
+/*
+ * or_moments — particle moments deposited on the nodes, PAPER.md:591 ("any particle-to-grid
+ * scatter operation ... standard charge and current deposition (four quantities per particle in
+ * 3D) ... the Implicit Moment Method (ten quantities per particle)"):
+ *
+ *   mom[g][m] = sigma * sum_p Q_p^m W_pg          (eq_shape_bspline weights)
+ *   Q_p = q_p (1, vx, vy, vz)                                              nq = 4  (rho, J)
+ *   Q_p = q_p (1, vx, vy, vz, vx vx, vx vy, vx vz, vy vy, vy vz, vz vz)    nq = 10 (implicit
+ *         moments: rho, J and the second-moment tensor, upper triangle row-major; reading R20)
+ *
+ * Plain per-particle loop over the support nodes in input order.  Whole periodic domain.
+ * out: [nodes][nq].  v: [np][3].
+ */
+int or_moments(const or_grid *g, int order, int nq, double sigma, int64_t np, const double *pos,
+               const double *q, const double *v, double *out, int accumulate)
+{
+    const int N1 = order + 1;
+    int64_t nn, p;
+    int rc = check_grid(g, order);
+    if (rc)
+        return rc;
+    if ((nq != 4 && nq != 10) || !v)
+        return OR_ERR_INVALID_ARG;
+    if (g->x_begin != 0 || g->x_end != g->n[0])
+        return OR_ERR_INVALID_ARG;
+    nn = (int64_t)g->n[0] * g->n[1] * g->n[2];
+    if (!accumulate)
+        memset(out, 0, sizeof(double) * (size_t)(nn * nq));
+    for (p = 0; p < np; ++p) {
+        int32_t cell[3], base[3];
+        double xi[3], w[3][3], Q[10];
+        const double *vp = v + 3 * p;
+        int mu, ax, ay, az, m;
+        rc = or_locate(g, pos + 3 * p, cell, xi);
+        if (rc)
+            return rc;
+        if (!isfinite(q[p]) || !isfinite(vp[0]) || !isfinite(vp[1]) || !isfinite(vp[2]))
+            return OR_ERR_NONFINITE;
+        for (mu = 0; mu < 3; ++mu)
+            or_support_1d(order, xi[mu], &base[mu], w[mu]);
+        Q[0] = 1.0;
+        Q[1] = vp[0];
+        Q[2] = vp[1];
+        Q[3] = vp[2];
+        Q[4] = vp[0] * vp[0];
+        Q[5] = vp[0] * vp[1];
+        Q[6] = vp[0] * vp[2];
+        Q[7] = vp[1] * vp[1];
+        Q[8] = vp[1] * vp[2];
+        Q[9] = vp[2] * vp[2];
+        for (m = 0; m < nq; ++m)
+            Q[m] = sigma * q[p] * Q[m];
+        for (ax = 0; ax < N1; ++ax)
+            for (ay = 0; ay < N1; ++ay)
+                for (az = 0; az < N1; ++az) {
+                    double Wa = w[0][ax] * w[1][ay] * w[2][az];
+                    int64_t ga = ((int64_t)wrap(cell[0] + base[0] + ax, g->n[0]) * g->n[1] +
+                                  wrap(cell[1] + base[1] + ay, g->n[1])) * g->n[2] +
+                                 wrap(cell[2] + base[2] + az, g->n[2]);
+                    for (m = 0; m < nq; ++m)
+                        out[ga * nq + m] += Q[m] * Wa;
+                }
+    }
+    return OR_OK;
+}
+
+/*
+ * or_gather — a nodal field interpolated to the particle positions, PAPER.md:96 ("B(x_p) being
+ * the magnetic field interpolated to the particle position"), with the same shape functions:
+ *
+ *   Fp[p][i] = sum_g W_pg F[g][i],   i < ncomp      (F: [nodes][ncomp], Fp: [np][ncomp])
+ *
+ * The nodal field lives on the nodes x_g = g h (reading R1) of the whole periodic domain.
+ */
+int or_gather(const or_grid *g, int order, int ncomp, int64_t np, const double *pos, const double *F,
+              double *Fp)
+{
+    const int N1 = order + 1;
+    int64_t p;
+    int rc = check_grid(g, order);
+    if (rc)
+        return rc;
+    if (ncomp < 1 || ncomp > 16)
+        return OR_ERR_INVALID_ARG;
+    if (g->x_begin != 0 || g->x_end != g->n[0])
+        return OR_ERR_INVALID_ARG;
+    for (p = 0; p < np; ++p) {
+        int32_t cell[3], base[3];
+        double xi[3], w[3][3];
+        int mu, ax, ay, az, i;
+        rc = or_locate(g, pos + 3 * p, cell, xi);
+        if (rc)
+            return rc;
+        for (mu = 0; mu < 3; ++mu)
+            or_support_1d(order, xi[mu], &base[mu], w[mu]);
+        for (i = 0; i < ncomp; ++i)
+            Fp[p * ncomp + i] = 0.0;
+        for (ax = 0; ax < N1; ++ax)
+            for (ay = 0; ay < N1; ++ay)
+                for (az = 0; az < N1; ++az) {
+                    double Wa = w[0][ax] * w[1][ay] * w[2][az];
+                    int64_t ga = ((int64_t)wrap(cell[0] + base[0] + ax, g->n[0]) * g->n[1] +
+                                  wrap(cell[1] + base[1] + ay, g->n[1])) * g->n[2] +
+                                 wrap(cell[2] + base[2] + az, g->n[2]);
+                    for (i = 0; i < ncomp; ++i)
+                        Fp[p * ncomp + i] += Wa * F[ga * ncomp + i];
+                }
+    }
+    return OR_OK;
+}

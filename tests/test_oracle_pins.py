@@ -467,3 +467,78 @@ def test_assemble_omp_equals_serial(order, n):
     a = oracle.assemble(n, order, 1, dl["pos"], dl["q"])
     b, _ = oracle.assemble_omp(n, order, 1, dl["pos"], dl["q"])
     assert (a == b).all()
+
+
+# ------------------------------------------------- NEXT-4: moments and field gather
+def test_moments_single_particle_hand_values():
+    # CIC, grid 4^3, x = (1.25, 2.5, 3.75), q = 2, v = (1, -2, 1/2): weights x {1: 3/4, 2: 1/4},
+    # y {2: 1/2, 3: 1/2}, z {3: 1/4, 0: 3/4} (z wraps).  At node (1, 2, 3): W = 3/32, rho = q W = 3/16,
+    # J = rho v = (3/16, -3/8, 3/32), second moments rho (vx vx, vx vy, vx vz, vy vy, vy vz, vz vz)
+    # = (3/16, -3/8, 3/32, 3/4, -3/16, 3/64); 8 nonzero nodes, total charge q
+    n = (4, 4, 4)
+    m = oracle.moments(n, 1, 10, [[1.25, 2.5, 3.75]], [2.0], [[1.0, -2.0, 0.5]])
+    exp = [Fraction(3, 16), Fraction(3, 16), Fraction(-3, 8), Fraction(3, 32), Fraction(3, 16), Fraction(-3, 8),
+           Fraction(3, 32), Fraction(3, 4), Fraction(-3, 16), Fraction(3, 64)]
+    assert [Fraction(x) for x in m[lin((1, 2, 3), n)]] == exp
+    assert np.count_nonzero(m[:, 0]) == 8 and m[:, 0].sum() == 2.0
+    m4 = oracle.moments(n, 1, 4, [[1.25, 2.5, 3.75]], [2.0], [[1.0, -2.0, 0.5]])
+    assert (m4 == m[:, :4]).all()
+    # TSC: x = (1.25, 2.5, 3.75) on 5^3: x {0: 1/32, 1: 11/16, 2: 9/32}, y {2: 1/2, 3: 1/2},
+    # z {3: 9/32, 4: 11/16, 0: 1/32}; rho at (1, 3, 4) = 2 (11/16)(1/2)(11/16) = 121/256
+    m2 = oracle.moments((5, 5, 5), 2, 4, [[1.25, 2.5, 3.75]], [2.0], [[1.0, -2.0, 0.5]])
+    assert Fraction(m2[lin((1, 3, 4), (5, 5, 5)), 0]) == Fraction(121, 256)
+    assert Fraction(m2[lin((1, 3, 4), (5, 5, 5)), 2]) == Fraction(-121, 128)
+
+
+@pytest.mark.parametrize("order,n", [(1, (4, 5, 3)), (2, (5, 6, 5)), (2, (7, 5, 6))])
+def test_moments_dense_and_totals(order, n):
+    # mom = W^T Q with the dense periodic W of the explicit B-spline definition (eq_weight_matrix)
+    d = synth.random_particles(n, 300, seed=17 + order, qrange=(-1.5, 1.5))
+    v = np.random.default_rng(3).uniform(-2, 2, (300, 3))
+    m = oracle.moments(n, order, 10, d["pos"], d["q"], v, sigma=0.5)
+    W = dense_W(n, d["pos"], order)
+    Q = d["q"][:, None] * np.column_stack([np.ones(300), v, v[:, 0] * v[:, 0], v[:, 0] * v[:, 1], v[:, 0] * v[:, 2],
+                                          v[:, 1] * v[:, 1], v[:, 1] * v[:, 2], v[:, 2] * v[:, 2]])
+    ref = 0.5 * W @ Q
+    assert np.abs(m - ref).max() <= 1e-13 * np.abs(Q).max() * 8
+    # partition of unity: sum over nodes = sigma sum_p Q_p
+    assert np.allclose(m.sum(0), 0.5 * Q.sum(0), rtol=1e-13, atol=1e-13 * np.abs(Q).sum())
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_charge_density_is_scalar_mass_row_sum(order):
+    # rho_g = sum_p q_p W_pg = sum_{g'} M_{gg'} of the scalar mass matrix (partition of unity,
+    # PAPER.md:164, applied to the pinned assembly)
+    n = (6, 5, 7)
+    d = _cfg_particles(order)
+    v = np.zeros_like(d["pos"])
+    rho = oracle.moments(n, order, 4, d["pos"], d["q"], v)[:, 0]
+    M = oracle.assemble(n, order, 1, d["pos"], d["q"])
+    assert np.allclose(rho, M[:, :, 0].sum(1), rtol=1e-13, atol=1e-14)
+
+
+@pytest.mark.parametrize("order", [1, 2])
+def test_gather_dense_constant_linear_and_adjoint(order):
+    n = (6, 7, 5)
+    rng = np.random.default_rng(9 + order)
+    d = synth.random_particles(n, 400, seed=23 + order)
+    nn = int(np.prod(n))
+    F = rng.standard_normal((nn, 3))
+    Fp = oracle.gather(n, order, d["pos"], F)
+    W = dense_W(n, d["pos"], order)
+    assert np.abs(Fp - W.T @ F).max() <= 1e-13 * np.abs(F).max() * 8
+    # a constant field is reproduced (partition of unity)
+    Fc = np.tile([1.5, -0.25, 3.0], (nn, 1))
+    assert np.abs(oracle.gather(n, order, d["pos"], Fc) - [1.5, -0.25, 3.0]).max() <= 1e-14
+    # a linear field is reproduced exactly by both B-splines away from the periodic seam
+    nl = (10, 9, 11)
+    gs = np.stack(np.meshgrid(*[np.arange(k) for k in nl], indexing="ij"), -1).reshape(-1, 3).astype(float)
+    A = np.array([[0.5, 1.0, 0.0], [-1.0, 0.25, 2.0], [0.0, 3.0, -0.5]])
+    Fl = gs @ A + [1.0, 2.0, 3.0]
+    xp = 2.0 + rng.random((300, 3)) * (np.array(nl) - 5.0)      # support windows never wrap
+    assert np.abs(oracle.gather(nl, order, xp, Fl) - (xp @ A + [1.0, 2.0, 3.0])).max() <= 1e-12
+    # adjointness: the gather is the transpose of the deposit, sum_p F(x_p).(q v)_p = sum_g F_g.J_g
+    v = rng.uniform(-1, 1, (400, 3))
+    J = oracle.moments(n, order, 4, d["pos"], d["q"], v)[:, 1:4]
+    lhs = np.sum(Fp * d["q"][:, None] * v)
+    assert abs(lhs - np.sum(F * J)) <= 1e-12 * np.sum(np.abs(F).max() * np.abs(d["q"][:, None] * v))
