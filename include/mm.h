@@ -184,6 +184,42 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
                       int accumulate, void *out, void *ghost, void *stream);
 
 /*
+ * mm_deposit_moments — particle moments on the nodes with the assembly's machinery (SURVEY.md
+ * NEXT-4; "any particle-to-grid scatter operation, where one MMA operand encodes
+ * the deposited quantities and the other encodes the interpolation weights"):
+ *   mom[g][m] = sigma * sum_p Q_p^m W_pg
+ *   nq = 4:  Q_p = q_p (1, vx, vy, vz)                                    (charge, current)
+ *   nq = 10: Q_p = q_p (1, vx, vy, vz, vx vx, vx vy, vx vz, vy vy, vy vz, vz vz)   (implicit
+ *            moment method quantities; second moments upper triangle row-major)
+ * per support-window bin on FP64 DMMA tiles (A = node weights, B = quantities).
+ *   h      sorted handle (with or without B); the particles are those given to the sort
+ *   sp     host; only sigma is used
+ *   v      device, [np][3] FP64 velocities in the caller's particle order (the order given to
+ *          mm_sort_by_cell; read through the handle's permutation)
+ *   accumulate 0: out = mom; 1: out += mom
+ *   out    device, FP64 [(x_end-x_begin)*n1*n2][nq] (node rows as in mm_assemble)
+ *   ghost  device, FP64 [mm_ghost_planes(order)*n1*n2][nq] for slab grids (zeroed unless
+ *          accumulate), NULL for the whole domain; reduced like the mass matrix's ghost planes
+ * Asynchronous.
+ */
+mm_status mm_deposit_moments(const mm_sorted *h, int nq, const mm_species *sp, const double *v, int accumulate,
+                             double *out, double *ghost, void *stream);
+
+/*
+ * mm_gather_field — a nodal vector field interpolated to the sorted particles with the same
+ * B-spline weights ("B(x_p) ... the magnetic field interpolated to the particle
+ * position"):  F_p = sum_g W_pg F_g.  The result REPLACES the B fields of the handle's records,
+ * so a following mm_assemble uses it (gather -> alpha -> mass matrix, no re-sort), and, if Fp is
+ * not NULL, is also written in the caller's particle order.
+ *   h      handle sorted WITH B (MM_ERR_INCOMPATIBLE otherwise); modified in place
+ *   F      device, FP64 [n0*n1*n2][3], the field at every node of the whole periodic domain
+ *          (also for a slab handle: the window of a bin may reach one plane beyond the slab)
+ *   Fp     device, FP64 [np][3] in the order given to mm_sort_by_cell, or NULL
+ * Asynchronous.
+ */
+mm_status mm_gather_field(mm_sorted *h, const double *F, double *Fp, void *stream);
+
+/*
  * mm_apply — y (+)= M E: the matrix-free product of an assembled FP64 mass
  * matrix with a nodal field, the operation the implicit field solve performs
  * with it ((L + sum_s M_s) E = b, eq_field_eq):

@@ -36,7 +36,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
 EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
-           "mm_assemble_slab", "mm_apply", "mm_ghost_add", "mm_ghost_exchange", "mm_ghost_planes", "mm_out_elems",
+           "mm_assemble_slab", "mm_deposit_moments", "mm_gather_field", "mm_apply", "mm_ghost_add", "mm_ghost_exchange", "mm_ghost_planes", "mm_out_elems",
            "mm_comm_unique_id", "mm_comm_create", "mm_comm_free", "mm_free", "mm_last_error", "mm_version",
            "mm_launch_count"]
 
@@ -96,6 +96,10 @@ def load_library(build_if_missing: bool = True):
     lib.mm_ghost_planes.restype = I
     lib.mm_out_elems.argtypes = [P, I, I]
     lib.mm_out_elems.restype = I64
+    lib.mm_deposit_moments.argtypes = [P, I, P, P, I, P, P, P]
+    lib.mm_deposit_moments.restype = I
+    lib.mm_gather_field.argtypes = [P, P, P, P]
+    lib.mm_gather_field.restype = I
     lib.mm_assemble_slab.argtypes = [P, I, I, P, I, P, P, P, P]
     lib.mm_assemble_slab.restype = I
     lib.mm_ghost_exchange.argtypes = [P, P, I, I, I, P, P, P]
@@ -245,6 +249,33 @@ def mm_assemble(handle: Sorted, kind: int, prec: int, species: mm_species, out, 
                          _stream_ptr(stream))
     _check(st)
     return out
+
+
+def moments_shape(grid: mm_grid, nq: int):
+    return ((grid.x_end - grid.x_begin) * grid.n[1] * grid.n[2], int(nq))
+
+
+def moments_ghost_shape(grid: mm_grid, order: int, nq: int):
+    return (load_library().mm_ghost_planes(order) * grid.n[1] * grid.n[2], int(nq))
+
+
+def mm_deposit_moments(handle: Sorted, nq: int, species: mm_species, v, out, ghost=None, accumulate: bool = False,
+                       stream=None):
+    """rho, J (nq = 4) or the 10 implicit-moment quantities per node (include/mm.h); v in the
+    particle order given to mm_sort_by_cell."""
+    _check(load_library().mm_deposit_moments(handle.ptr, int(nq), ctypes.byref(species),
+                                             _dev_ptr(v, name="v") if v is not None else None,
+                                             int(bool(accumulate)), _dev_ptr(out, name="out"),
+                                             _dev_ptr(ghost, name="ghost") if ghost is not None else None,
+                                             _stream_ptr(stream)))
+    return out
+
+
+def mm_gather_field(handle: Sorted, F, Fp=None, stream=None):
+    """F at the sorted particles -> the handle's B fields (and Fp in the caller's order)."""
+    _check(load_library().mm_gather_field(handle.ptr, _dev_ptr(F, name="F"),
+                                          _dev_ptr(Fp, name="Fp") if Fp is not None else None, _stream_ptr(stream)))
+    return Fp
 
 
 def mm_ghost_add(grid: mm_grid, order: int, kind: int, out, recv, first_plane: int, nplanes: int, stream=None):

@@ -543,6 +543,59 @@ mm_status mm_assemble_slab(const mm_sorted *h, mm_kind kind, mm_precision prec, 
     }
 }
 
+mm_status mm_deposit_moments(const mm_sorted *h, int nq, const mm_species *sp, const double *v, int accumulate,
+                             double *out, double *ghost, void *stream)
+{
+    try {
+        if (!h || !sp || !out || (h->np > 0 && !v))
+            return fail(MM_ERR_INVALID_ARG, "NULL handle, species, v or out");
+        if (!h->valid)
+            return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
+        if (nq != 4 && nq != 10)
+            return fail(MM_ERR_INVALID_ARG, "nq must be 4 (rho, J) or 10 (implicit moments)");
+        if (!std::isfinite(sp->sigma))
+            return fail(MM_ERR_INVALID_ARG, "sigma must be finite");
+        mm::Geo geo = mm::make_geo(h->g, h->order);
+        if (!geo.periodic_x && !ghost)
+            return fail(MM_ERR_INVALID_ARG, "slab grid needs a ghost buffer");
+        cudaStream_t s = (cudaStream_t)stream;
+        const int64_t plane = (int64_t)h->g.n[1] * h->g.n[2] * nq;
+        cudaError_t e = cudaSuccess;
+        if (!accumulate) {
+            e = cudaMemsetAsync(out, 0, sizeof(double) * (size_t)((h->g.x_end - h->g.x_begin) * plane), s);
+            if (!e && !geo.periodic_x)
+                e = cudaMemsetAsync(ghost, 0, sizeof(double) * (size_t)(mm_ghost_planes(h->order) * plane), s);
+        }
+        if (!e)
+            e = mm::moments_enqueue(geo, nq, h->rec, h->has_B ? 8 : 4, h->perm, h->seg_begin, h->nbins, v, sp->sigma,
+                                    out, geo.periodic_x ? nullptr : ghost, s);
+        if (e)
+            return cuda_fail(e, "mm_deposit_moments");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_deposit_moments");
+    }
+}
+
+mm_status mm_gather_field(mm_sorted *h, const double *F, double *Fp, void *stream)
+{
+    try {
+        if (!h || !F)
+            return fail(MM_ERR_INVALID_ARG, "NULL handle or field");
+        if (!h->valid)
+            return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
+        if (!h->has_B && h->np > 0)
+            return fail(MM_ERR_INCOMPATIBLE, "the gather writes B into the records: sort with B");
+        mm::Geo geo = mm::make_geo(h->g, h->order);
+        cudaError_t e = mm::gather_enqueue(geo, h->rec, h->perm, h->seg_begin, h->nbins, F, Fp, (cudaStream_t)stream);
+        if (e)
+            return cuda_fail(e, "mm_gather_field");
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_gather_field");
+    }
+}
+
 mm_status mm_apply(const mm_grid *g, int order, mm_kind kind, const double *M, const double *E, double *y,
                    int accumulate, void *stream)
 {

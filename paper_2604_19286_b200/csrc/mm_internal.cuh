@@ -77,6 +77,13 @@ cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cuda
 cudaError_t apply_enqueue(const Geo &geo, int ncomp, const double *M, const double *E, double *y, int accumulate,
                           cudaStream_t s);
 
+// ---- NEXT-4: moments and field gather (mm_moments.cu) -------------------------
+cudaError_t moments_enqueue(const Geo &g, int nq, const double *rec, int rs, const int32_t *perm,
+                            const int32_t *seg_begin, int64_t nbins, const double *v, double sigma, double *out,
+                            double *ghost, cudaStream_t s);
+cudaError_t gather_enqueue(const Geo &g, double *rec, const int32_t *perm, const int32_t *seg_begin, int64_t nbins,
+                           const double *F, double *Fp, cudaStream_t s);
+
 // ---- communicator (mm_comm.cu) -----------------------------------------------
 mm_status api_fail(mm_status st, const char *fmt, ...);  // sets mm_last_error (mm_api.cu)
 const char *nccl_error(int r);
