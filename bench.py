@@ -573,7 +573,7 @@ def main():
                 del r
         line["tf32"] = tf
 
-    # ---- c2 with the production storage of PAPER.md:576 (NEXT-2): FP32 positions and B, FP64
+    # ---- c2 with the production storage of PAPER.md:572 (NEXT-2): FP32 positions and B, FP64
     #      charges and mass matrix; sort + FP64 assembly per step
     if world == 1:
         cfg2 = synth.config("c2")
@@ -608,7 +608,7 @@ def main():
             stm["h"] = mm.mm_sort_by_cell(gm, 1, 4, dm["pos"], dm["q"], dm["B"], handle=stm["h"])
         q1.record()
         barrier()
-        line["mixed_inputs"] = {"workload": "c2 with FP32 positions and B, FP64 q and mass matrix (PAPER.md:576)",
+        line["mixed_inputs"] = {"workload": "c2 with FP32 positions and B, FP64 q and mass matrix (PAPER.md:572)",
                                 "value": len(d2["q"]) / (tm / 1e3) / 1e6, "unit": UNIT, "ms_per_step": tm,
                                 "sort_ms": q0.elapsed_time(q1) / nm, "input_bytes_per_particle": 32}
         mm.mm_free(stm["h"])
@@ -842,7 +842,7 @@ def main():
                        "d2h_bytes_per_step": host_out.numel() * 8, "steps": ke, "host_copy_matches_device": e2e_ok,
                        "note": "pinned host pos/q/B -> device, sort + assemble, full mass matrix -> pinned host; "
                                "pipelined across steps (H2D of k+1 and D2H of k-1 overlap step k)"}
-        # the same end-to-end pipeline with the production storage of PAPER.md:576 (FP32 positions
+        # the same end-to-end pipeline with the production storage of PAPER.md:572 (FP32 positions
         # and B, mm_sort_by_cell_mixed): half the H2D bytes of the inputs
         if world == 1 and "mixed_inputs" in line:
             p32 = d["pos"].astype(np.float32)

@@ -138,7 +138,7 @@ mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, co
                           const double *q, const double *B, void *stream, mm_sorted **inout);
 
 /*
- * mm_sort_by_cell_mixed — the same sort for the production storage of PAPER.md:576
+ * mm_sort_by_cell_mixed — the same sort for the production storage of PAPER.md:572
  * ("field values and particle positions are stored in FP32, while ... statistical
  * weights and the mass matrix use FP64"): pos and B are FP32 ([np][3] each, B may be
  * NULL), q is FP64.  Every value is widened exactly to FP64 before locate (R5), so the

@@ -173,7 +173,7 @@ class Sorted:
 def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handle: Sorted | None = None,
                     stream=None) -> Sorted:
     """Stable support-window binning with K-padding (include/mm.h).  Reuses `handle` if given.
-    FP32 pos (and B) select mm_sort_by_cell_mixed (PAPER.md:576 storage; q stays FP64)."""
+    FP32 pos (and B) select mm_sort_by_cell_mixed (PAPER.md:572 storage; q stays FP64)."""
     lib = load_library()
     f32 = pos is not None and pos.dtype == torch.float32
     np_ = int(pos.shape[0]) if pos is not None else 0

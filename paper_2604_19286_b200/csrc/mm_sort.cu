@@ -97,7 +97,7 @@ __device__ __forceinline__ void load_vec3x4(const double *__restrict__ a, int64_
     }
 }
 
-// FP32 variant (mixed-precision inputs, PAPER.md:576): three 16-B loads, widened exactly.
+// FP32 variant (mixed-precision inputs, PAPER.md:572): three 16-B loads, widened exactly.
 template <bool VEC>
 __device__ __forceinline__ void load_vec3x4(const float *__restrict__ a, int64_t p0, int64_t np, double v[12])
 {

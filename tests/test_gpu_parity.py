@@ -508,7 +508,7 @@ def test_sort_scalar_handle_records(order):
 # ------------------------------------------------------------- mixed-precision inputs (NEXT-2)
 @pytest.mark.parametrize("order", [1, 2])
 def test_mixed_precision_inputs(order):
-    # FP32 positions and B, FP64 charges (PAPER.md:576): the sort and the FP64 assembly equal the
+    # FP32 positions and B, FP64 charges (PAPER.md:572): the sort and the FP64 assembly equal the
     # oracle run on the exactly widened arrays (sort bit-exact, entries <= 1e-12)
     m = mm()
     n = (7, 6, 5)

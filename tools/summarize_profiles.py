@@ -33,6 +33,11 @@ METRICS = [
     ("lts__d_atomic_input_cycles_active.avg.pct_of_peak_sustained_elapsed", "L2 atomic input % active"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem bank conflicts"),
     ("smsp__inst_executed.sum", "warp instructions"),
+    ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe % active (tcgen05)"),
+    ("sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum", "UTCHMMA TF32 ops"),
+    ("sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed",
+     "UTCHMMA TF32 % of peak"),
+    ("smsp__sass_inst_executed_op_utcmma.sum", "tcgen05.mma instructions"),
 ]
 
 
@@ -69,12 +74,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     ap.add_argument("--src", default="gpurun_out")
-    ap.add_argument("--reps", nargs="*", default=["prof_asm1", "prof_asm2", "prof_sort"])
+    ap.add_argument("--reps", nargs="*", default=["prof_c2", "prof_c3", "prof_tf32", "prof_c4o2", "prof_apply", "prof_sort"])
     a = ap.parse_args()
     os.makedirs("profiles", exist_ok=True)
     lines = [f"# ncu summary ({a.round})", "",
              "Captured with `ncu --set full --clock-control none --import-source on` on one B200 "
-             "(gpurun), kernels of `bench.py` (c2 / c3).  Values per launch.", ""]
+             "(gpurun), kernels of `tools/gpu_round.sh` (bench.py / tools timing scripts on c2, c3, c4).  Values per launch.", ""]
     traffic = {}
     for rep in a.reps:
         path = os.path.join(a.src, rep + ".ncu-rep")
