@@ -35,6 +35,8 @@ struct mm_sorted {
     int32_t *d_status;
     int32_t *h_status;  // pinned
     int32_t *d_work;    // assembly work counter
+    int32_t *d_flags;   // first-writer zeroing: one flag per output node row (lazily allocated)
+    int32_t epoch;      // flag value of the last zeroing launch
 };
 
 namespace {
@@ -98,6 +100,7 @@ void release(mm_sorted *h)
     cudaFree(h->huge_list);
     cudaFree(h->d_status);
     cudaFree(h->d_work);
+    cudaFree(h->d_flags);
     if (h->h_status)
         cudaFreeHost(h->h_status);
     delete h;
@@ -361,7 +364,8 @@ mm_status check_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, co
 // mm_assemble; boundary / interior ranges for mm_assemble_slab).  work_idx selects the launch's
 // work counter (zeroed by the caller).
 cudaError_t enqueue_range(const mm_sorted *h, mm::Geo geo, mm_kind kind, mm_precision prec, const mm_species *sp,
-                          void *out, void *ghost, int bx_lo, int bx_hi, int work_idx, cudaStream_t s)
+                          void *out, void *ghost, int bx_lo, int bx_hi, int work_idx, cudaStream_t s,
+                          int32_t *zflags = nullptr, int32_t zepoch = 0)
 {
     const int64_t plane = (int64_t)h->g.n[1] * h->g.n[2];
     if (bx_hi <= bx_lo)
@@ -378,6 +382,8 @@ cudaError_t enqueue_range(const mm_sorted *h, mm::Geo geo, mm_kind kind, mm_prec
     a.sigma = sp->sigma;
     a.out = static_cast<double *>(out);
     a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
+    a.zflags = zflags;
+    a.zepoch = zepoch;
     if (prec == MM_FP64)
         return mm::assemble_fp64_enqueue(geo, a, s);
     return mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);
@@ -422,7 +428,27 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         const int64_t nout = (int64_t)(h->g.x_end - h->g.x_begin) * h->g.n[1] * h->g.n[2] * rowlen;
         const int64_t nghost = geo.periodic_x ? 0 : (int64_t)mm_ghost_planes(h->order) * h->g.n[1] * h->g.n[2] * rowlen;
         cudaError_t e = cudaSuccess;
-        if (!accumulate) {
+        // kernels that zero their output rows themselves (first-writer flags)
+        int32_t *zflags = nullptr;
+        if (!accumulate && mm::zeroes_inside(h->order, (int)kind, prec == MM_FP64 ? 0 : 1)) {
+            mm_sorted *hm = const_cast<mm_sorted *>(h);
+            if (!hm->d_flags) {
+                e = cudaMalloc((void **)&hm->d_flags, sizeof(int32_t) * (size_t)mm::flag_rows(h->g, h->order));
+                if (!e)
+                    e = cudaMemsetAsync(hm->d_flags, 0, sizeof(int32_t) * (size_t)mm::flag_rows(h->g, h->order), s);
+                if (e)
+                    return cuda_fail(e, "mm_assemble flags");
+                hm->epoch = 0;
+            }
+            if (++hm->epoch == INT32_MAX) {  // flags restart from 0 after 2^31 launches
+                e = cudaMemsetAsync(hm->d_flags, 0, sizeof(int32_t) * (size_t)mm::flag_rows(h->g, h->order), s);
+                if (e)
+                    return cuda_fail(e, "mm_assemble flags");
+                hm->epoch = 1;
+            }
+            zflags = hm->d_flags;
+        }
+        if (!accumulate && !zflags) {
             e = cudaMemsetAsync(out, 0, esz * (size_t)nout, s);
             if (!e && nghost)
                 e = cudaMemsetAsync(ghost, 0, esz * (size_t)nghost, s);
@@ -432,7 +458,7 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
         if (e)
             return cuda_fail(e, "mm_assemble memset");
-        e = enqueue_range(h, geo, kind, prec, sp, out, ghost, 0, geo.nbx, 0, s);
+        e = enqueue_range(h, geo, kind, prec, sp, out, ghost, 0, geo.nbx, 0, s, zflags, zflags ? h->epoch : 0);
         if (e)
             return cuda_fail(e, "mm_assemble launch");
         return MM_OK;

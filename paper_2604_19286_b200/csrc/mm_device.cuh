@@ -43,6 +43,21 @@ __device__ __forceinline__ void red_add(double *p, double v)
     asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
+// The same without a compiler memory clobber: shared-memory loads may be scheduled across it
+// (the RED reads only registers; ordering against later global writes and flag releases is
+// kept by asm volatile order and the release's own clobber).
+__device__ __forceinline__ void red_add_nc(double *p, double v)
+{
+    asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v));
+}
+
+// Predicated form (one instruction, no branch around it).
+__device__ __forceinline__ void red_add_if(double *p, double v, bool ok)
+{
+    asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q red.global.add.f64 [%0], %1;\n\t}" ::"l"(p),
+                 "d"(v), "r"((int)ok));
+}
+
 __device__ __forceinline__ int wrapi(int i, int n)
 {
     return i < 0 ? i + n : (i >= n ? i - n : i);
@@ -60,6 +75,112 @@ __device__ __forceinline__ double *row_ptr(const Geo &g, int X, int Y, int Z, do
         return out + ((int64_t)(xl * g.n1 + Y) * g.n2 + Z) * rowlen;
     int plane = (g.order == 1) ? 0 : (X < g.x_begin ? 0 : 1 + (X - g.x_end));
     return ghost + ((int64_t)(plane * g.n1 + Y) * g.n2 + Z) * rowlen;
+}
+
+// Flag index of a node row (same X convention as row_ptr): owned rows first, then the ghost
+// planes in row_ptr's order.
+__device__ __forceinline__ int64_t row_id(const Geo &g, int X, int Y, int Z)
+{
+    if (g.periodic_x) {
+        X = X < 0 ? X + g.n0 : (X >= g.n0 ? X - g.n0 : X);
+        return ((int64_t)X * g.n1 + Y) * g.n2 + Z;
+    }
+    const int xl = X - g.x_begin;
+    if (xl >= 0 && X < g.x_end)
+        return ((int64_t)xl * g.n1 + Y) * g.n2 + Z;
+    const int plane = (g.order == 1) ? 0 : (X < g.x_begin ? 0 : 1 + (X - g.x_end));
+    return ((int64_t)(g.x_end - g.x_begin + plane) * g.n1 + Y) * g.n2 + Z;
+}
+
+// ---- first-writer zeroing (DESIGN.md §7 "Output zeroing inside the assembly") -----------
+// Bins are processed in DESCENDING index order through a ticket counter (ticket t = bin
+// nbins-1-t), so the first bin to touch a node row is the toucher with the largest index.
+// The holder of ticket t zeroes the rows whose first toucher is ticket t + D (and, for t < D,
+// those of ticket t itself) as soon as it has the ticket (not when it processes it: a ticket
+// held for later must not hold back rows others wait for), and publishes them (flag = epoch,
+// release) before its next wait; a bin waits (acquire) for the flags of the rows it deposits
+// into.  Every waiter's rows are zeroed by a ticket taken no later than its own, by a running
+// warp that releases before it waits: no deadlock, whatever the residency.
+struct ZeroPlan {
+    int32_t *flags;  // [rows owned + ghost rows]; nullptr: no zeroing in the kernel
+    int32_t epoch;   // this launch's flag value (the handle counts launches)
+    int lookahead;   // D, in tickets
+};
+
+// Row coordinates along one axis whose first toucher (largest covering bin) is bin coordinate
+// b; bins b in [0, nb) cover rows b - s + a, a = 0..R (mod n when periodic; then nb = n + s).
+// Periodic: a row u < R is first touched by the last bin nb - 1 (through the wrap), any other
+// row by bin u + s.  Slab (x, no wrap): row u by bin min(u + s, nb - 1).  Returns the count
+// (<= R + 1); u[] holds wrapped (periodic) or local unwrapped (slab) coordinates.
+__device__ __forceinline__ int first_rows(int b, int nb, int n, int R, int s, bool periodic, int u[3])
+{
+    if (b == nb - 1) {
+        if (periodic) {
+            u[0] = 0;
+            u[1] = R == 1 ? n - 1 : 1;
+            u[2] = n - 1;
+        } else {
+            u[0] = nb - 1 - s;
+            u[1] = nb - s;
+            u[2] = nb + 1 - s;
+        }
+        return R + 1;
+    }
+    if (periodic && b - s < R)
+        return 0;
+    u[0] = b - s;
+    return 1;
+}
+
+// Rows whose first toucher is bin `bin` (whole-range launch: bin planes 0..nbx-1): the per-axis
+// lists.  Returns the number of rows (product of the list lengths).
+__device__ __forceinline__ int first_rows3(const Geo &g, int bin, int ux[3], int uy[3], int uz[3], int &nx, int &ny,
+                                           int &nz)
+{
+    const int R = g.order, plane = g.n1 * g.n2;
+    const int bxl = bin / plane, rem = bin - bxl * plane, by = rem / g.n2, bz = rem - by * g.n2;
+    nx = first_rows(bxl, g.nbx, g.n0, R, R - 1, g.periodic_x != 0, ux);
+    ny = first_rows(by, g.n1, g.n1, R, 0, true, uy);
+    nz = first_rows(bz, g.n2, g.n2, R, 0, true, uz);
+    return nx * ny * nz;
+}
+
+// Warp-cooperative zeroing of the rows first touched by `bin`; lane lbase + k (k < count) gets
+// the flag index of row k in `rel` for the later release.
+__device__ __forceinline__ void zero_first_rows(const Geo &g, int bin, double *out, double *ghost, int rowlen, int lane,
+                                                int lbase, int64_t &rel)
+{
+    int ux[3], uy[3], uz[3], nx, ny, nz;
+    const int cnt = first_rows3(g, bin, ux, uy, uz, nx, ny, nz);
+    for (int k = 0; k < cnt; ++k) {
+        const int ix = k / (ny * nz), r = k - ix * ny * nz, iy = r / nz, iz = r - iy * nz;
+        const int X = g.x_begin + (ix == 0 ? ux[0] : (ix == 1 ? ux[1] : ux[2]));
+        const int Y = iy == 0 ? uy[0] : (iy == 1 ? uy[1] : uy[2]);
+        const int Z = iz == 0 ? uz[0] : (iz == 1 ? uz[1] : uz[2]);
+        double *p = row_ptr(g, X, Y, Z, out, ghost, rowlen);
+        for (int e = lane; e < rowlen; e += 32)
+            p[e] = 0.0;
+        if (lane == lbase + k)
+            rel = row_id(g, X, Y, Z);
+    }
+}
+
+__device__ __forceinline__ void flag_release(int32_t *p, int32_t v)
+{
+    asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int32_t flag_acquire(const int32_t *p)
+{
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void flag_wait(const int32_t *p, int32_t v)
+{
+    while (flag_acquire(p) != v) {
+    }
 }
 
 // s^{ij} = sigma q alpha^{ij}, alpha = (delta + omega omega^T + eps omega)/(1+|omega|^2)

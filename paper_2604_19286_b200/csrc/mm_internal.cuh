@@ -8,6 +8,15 @@
 
 namespace mm {
 
+// Node rows of a handle's output (owned rows + ghost planes): the size of the flag array of
+// the first-writer zeroing.
+inline int64_t flag_rows(const mm_grid &g, int order)
+{
+    const bool whole = g.x_begin == 0 && g.x_end == g.n[0];
+    const int planes = (g.x_end - g.x_begin) + (whole ? 0 : (order == 1 ? 1 : 3));
+    return (int64_t)planes * g.n[1] * g.n[2];
+}
+
 // Kernel-side grid/slab geometry.
 struct Geo {
     int n0, n1, n2;
@@ -67,8 +76,12 @@ struct AsmArgs {
     double *out;          // owned rows (FP64; FP32 for the TF32 paths, reinterpreted)
     double *ghost;        // ghost planes (slab only)
     int *work;            // device work counter, zeroed before the launch
+    int32_t *zflags;      // first-writer zeroing (dev::ZeroPlan): row flags, nullptr = output pre-zeroed
+    int32_t zepoch;       //   flag value of this launch
 };
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
+// true when the kernel for (order, ncomp, tf32) zeroes its output rows itself (AsmArgs::zflags)
+bool zeroes_inside(int order, int ncomp, int tf32);
 
 // ---- TF32 / 3xTF32 on tcgen05 (mm_assemble_tf32.cu); out/ghost hold FP32 ----------
 cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cudaStream_t s);
