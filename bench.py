@@ -538,6 +538,53 @@ def main():
                           "assemble_mps": r1["np"] / (r1["assemble_ms"] / 1e3) / 1e6},
             "apply": r1.get("apply")}
 
+    # ---- NEXT-4 on the c2 handle: moment deposition (rho, J: nq = 4; implicit-moment quantities:
+    #      nq = 10) on FP64 DMMA tiles and the B-field gather, each against the HBM roofline on its
+    #      algorithmic bytes: 32 B (xi, q of the record) + 4 B (perm) + 24 B (v, caller order) read
+    #      + nq x 8 B per node written once (moments); 32 + 4 B read + 24 B written (B in the record)
+    #      + 24 B (F_p, caller order) per particle (gather)
+    if world == 1:
+        h1, g1 = r1["state"]["h"], r1["grid"]
+        npart = r1["np"]
+        nnodes = cfg.n[0] * cfg.n[1] * cfg.n[2]
+        vdev = torch.rand(npart, 3, dtype=torch.float64, device=dev) - 0.5
+        nx4 = {}
+        reps4 = max(10, args.steps // 10)
+
+        def timed4(fn):
+            for _ in range(3):
+                fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record()
+            for _ in range(reps4):
+                fn()
+            e1.record()
+            barrier()
+            return e0.elapsed_time(e1) / reps4
+
+        for nq in (4, 10):
+            mo = torch.empty(mm.moments_shape(g1, nq), dtype=torch.float64, device=dev)
+            t = timed4(lambda: mm.mm_deposit_moments(h1, nq, mm.Species(), vdev, mo))
+            byts = npart * 60.0 + nnodes * nq * 8.0
+            nx4[f"moments_nq{nq}"] = {"ms": t, "mps": npart / (t / 1e3) / 1e6,
+                                      "roofline": {"bound": "hbm", "achieved": byts / (t / 1e3) / 1e9,
+                                                   "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                                   "frac": byts / (t / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.1),
+                                                   "alg_bytes_per_particle": 60.0 + nq * 8.0 / ppc}}
+            del mo
+        Fn = torch.rand(nnodes, 3, dtype=torch.float64, device=dev)
+        Fp = torch.empty(npart, 3, dtype=torch.float64, device=dev)
+        t = timed4(lambda: mm.mm_gather_field(h1, Fn, Fp))
+        byts = npart * 84.0 + nnodes * 24.0
+        nx4["gather"] = {"ms": t, "mps": npart / (t / 1e3) / 1e6,
+                         "roofline": {"bound": "hbm", "achieved": byts / (t / 1e3) / 1e9,
+                                      "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                                      "frac": byts / (t / 1e3) / 1e9 / peaks.get("hbm_gbs", 6535.1),
+                                      "alg_bytes_per_particle": 84.0 + 24.0 / ppc}}
+        del Fn, Fp, vdev
+        line["next4"] = dict(workload="c2 handle (16.8 M particles, 64^3 CIC)", **nx4)
+
     if not args.no_order2:
         r2 = measure("c3", True)
         F2 = flops_per_particle(2, 9)

@@ -1,7 +1,7 @@
-"""GPU: the assembly kernels that zero their own output rows (first-writer flags)
-leave no stale value behind, whatever the buffer held before, on whole and slab grids, across
-repeated launches on one handle (the flag epoch), with the lookahead both larger and smaller
-than the number of bins; accumulate=1 still adds to what the buffer holds."""
+"""GPU: mm_assemble (accumulate=0) leaves no stale value behind, whatever the buffer held before
+(the memset, or k_asm_o1t's in-kernel first-writer zeroing), on whole and slab
+grids, across repeated launches on one handle (the flag epoch), with the zeroing lookahead both
+larger and smaller than the number of bins; accumulate=1 still adds to what the buffer holds."""
 import numpy as np
 import pytest
 
@@ -86,3 +86,16 @@ def test_accumulate_keeps_prefill():
     m.mm_assemble(h, m.MM_TENSOR, m.MM_FP64, m.Species(), out, accumulate=1)
     torch.cuda.synchronize()
     assert rel_err(out.cpu().numpy(), 2 * ref) <= 1e-12
+
+
+def test_in_kernel_zeroing_subprocess():
+    """The same checks with k_asm_o1t's in-kernel first-writer zeroing switched on (MM_ZERO_O1=1,
+    read once per process, hence a child process); off by default (slower than the memset)."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, MM_ZERO_O1="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", os.path.abspath(__file__), "-q", "-x", "-m", "gpu",
+                        "-k", "not subprocess"], env=env, capture_output=True, text=True, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
