@@ -52,6 +52,46 @@ __device__ __forceinline__ void axis_weights(double xi, double w[3])
     }
 }
 
+// A warp's stream of 32-particle chunks over its bins (bin, bin + W, ...; empty bins skipped).
+struct ChunkIt {
+    int64_t bin;
+    int base, end;  // [base, end): this chunk's slots in the bin's segment; base == end: done
+};
+__device__ __forceinline__ ChunkIt first_chunk(int64_t bin, int64_t W, int64_t nbins, const int32_t *seg)
+{
+    for (; bin < nbins; bin += W) {
+        const int b0 = __ldg(seg + bin), b1 = __ldg(seg + bin + 1);
+        if (b1 > b0)
+            return {bin, b0, b1};
+    }
+    return {nbins, 0, 0};
+}
+__device__ __forceinline__ ChunkIt next_chunk(const ChunkIt &c, int64_t W, int64_t nbins, const int32_t *seg)
+{
+    if (c.base + 32 < c.end)
+        return {c.bin, c.base + 32, c.end};
+    return first_chunk(c.bin + W, W, nbins, seg);
+}
+
+// Per-lane inputs of one chunk: record (xi, q) and the permutation entry, loaded one chunk
+// ahead; the velocity (a dependent, random read through perm) is issued as soon as perm has
+// arrived, i.e. one chunk ahead as well but after the current chunk's compute.
+struct MoIn {
+    double4 r;  // xi x, y, z, q (zeros past the bin's end)
+    int p;      // caller index, -1 for padding / past the end
+};
+__device__ __forceinline__ MoIn load_mo(const ChunkIt &c, int lane, const double *rec, int rs, const int32_t *perm)
+{
+    MoIn in;
+    in.r = make_double4(0, 0, 0, 0);
+    in.p = -1;
+    if (c.base + lane < c.end) {
+        in.r = ld256(rec + (int64_t)rs * (c.base + lane));
+        in.p = __ldg(perm + c.base + lane);
+    }
+    return in;
+}
+
 template <int ORDER, int NQ>
 __global__ void __launch_bounds__(128) k_moments(Geo g, const double *__restrict__ rec, int rs,
                                                  const int32_t *__restrict__ perm,
@@ -76,89 +116,102 @@ __global__ void __launch_bounds__(128) k_moments(Geo g, const double *__restrict
     __syncwarp();
     const int kq = lane & 3, rq = lane >> 2;
     const int64_t W = (int64_t)gridDim.x * 4;
-    for (int64_t bin = blockIdx.x * 4 + warp; bin < nbins; bin += W) {
-        const int b0 = __ldg(seg_begin + bin), b1 = __ldg(seg_begin + bin + 1);
-        if (b1 == b0)
-            continue;
-        double acc[L::MT][NT][2];
+    // three-stage pipeline over the warp's chunks: records + perm two chunks ahead, the
+    // velocities (random reads through perm) one chunk ahead
+    auto load_v = [&](const MoIn &x) {
+        double3 r3 = make_double3(0, 0, 0);
+        if (x.p >= 0)
+            r3 = make_double3(__ldg(v + 3 * (int64_t)x.p), __ldg(v + 3 * (int64_t)x.p + 1),
+                              __ldg(v + 3 * (int64_t)x.p + 2));
+        return r3;
+    };
+    ChunkIt cur = first_chunk(blockIdx.x * 4 + warp, W, nbins, seg_begin);
+    ChunkIt nxt = next_chunk(cur, W, nbins, seg_begin);
+    MoIn in = load_mo(cur, lane, rec, rs, perm);
+    MoIn nin = load_mo(nxt, lane, rec, rs, perm);
+    double3 vv = load_v(in);
+    double acc[L::MT][NT][2];
 #pragma unroll
-        for (int i = 0; i < L::MT; ++i)
+    for (int i = 0; i < L::MT; ++i)
+#pragma unroll
+        for (int j = 0; j < NT; ++j)
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+    while (cur.bin < nbins) {
+        const ChunkIt nxt2 = next_chunk(nxt, W, nbins, seg_begin);
+        const MoIn nin2 = load_mo(nxt2, lane, rec, rs, perm);
+        const double3 nvv = load_v(nin);
+        const int m = min(32, cur.end - cur.base);
+        __syncwarp();  // the previous chunk's DMMAs / deposit are done with xz
+        {
+            double wx[3], wy[3], wz[3];
+            axis_weights<ORDER>(in.r.x, wx);
+            axis_weights<ORDER>(in.r.y, wy);
+            axis_weights<ORDER>(in.r.z, wz);
+            double *col = xz + lane;
+#pragma unroll
+            for (int a = 0; a < L::N; ++a) {
+                const int ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
+                          az = a % (ORDER + 1);
+                col[a * L::XS] = (wx[ax] * wy[ay]) * wz[az];
+            }
+            const double s = sigma * in.r.w;  // 0 past the bin's end / on padding records
+            const double vx = vv.x, vy = vv.y, vz = vv.z;
+            double Q[10] = {s, s * vx, s * vy, s * vz, 0, 0, 0, 0, 0, 0};
+            if (NQ == 10) {
+                Q[4] = s * (vx * vx), Q[5] = s * (vx * vy), Q[6] = s * (vx * vz);
+                Q[7] = s * (vy * vy), Q[8] = s * (vy * vz), Q[9] = s * (vz * vz);
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+                col[(8 * L::MT + q) * L::XS] = Q[q];
+        }
+        __syncwarp();
+        for (int kb = 0; kb < m; kb += 4) {
+            double bv[NT];
 #pragma unroll
             for (int j = 0; j < NT; ++j)
-                acc[i][j][0] = acc[i][j][1] = 0.0;
-        for (int base = b0; base < b1; base += 32) {
-            const int m = min(32, b1 - base);
-            double xi[3] = {0.0, 0.0, 0.0}, qq = 0.0, vx = 0.0, vy = 0.0, vz = 0.0;
-            if (lane < m) {
-                const double *r = rec + (int64_t)rs * (base + lane);
-                xi[0] = r[0], xi[1] = r[1], xi[2] = r[2], qq = r[3];
-                const int p = __ldg(perm + base + lane);
-                if (p >= 0) {
-                    vx = __ldg(v + 3 * (int64_t)p), vy = __ldg(v + 3 * (int64_t)p + 1), vz = __ldg(v + 3 * (int64_t)p + 2);
-                }
-            }
-            __syncwarp();
-            {
-                double wx[3], wy[3], wz[3];
-                axis_weights<ORDER>(xi[0], wx);
-                axis_weights<ORDER>(xi[1], wy);
-                axis_weights<ORDER>(xi[2], wz);
-                double *col = xz + lane;
+                bv[j] = xz[(8 * L::MT + 8 * j + rq) * L::XS + kb + kq];
 #pragma unroll
-                for (int a = 0; a < L::N; ++a) {
-                    const int ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
-                              az = a % (ORDER + 1);
-                    col[a * L::XS] = (wx[ax] * wy[ay]) * wz[az];
-                }
-                const double s = sigma * qq;  // 0 past the bin's end / on padding records
-                double Q[10] = {s, s * vx, s * vy, s * vz, 0, 0, 0, 0, 0, 0};
-                if (NQ == 10) {
-                    Q[4] = s * (vx * vx), Q[5] = s * (vx * vy), Q[6] = s * (vx * vz);
-                    Q[7] = s * (vy * vy), Q[8] = s * (vy * vz), Q[9] = s * (vz * vz);
-                }
-#pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    col[(8 * L::MT + q) * L::XS] = Q[q];
-            }
-            __syncwarp();
-            for (int kb = 0; kb < m; kb += 4) {
-                double bv[NT];
+            for (int i = 0; i < L::MT; ++i) {
+                const double av = xz[(8 * i + rq) * L::XS + kb + kq];
 #pragma unroll
                 for (int j = 0; j < NT; ++j)
-                    bv[j] = xz[(8 * L::MT + 8 * j + rq) * L::XS + kb + kq];
-#pragma unroll
-                for (int i = 0; i < L::MT; ++i) {
-                    const double av = xz[(8 * i + rq) * L::XS + kb + kq];
-#pragma unroll
-                    for (int j = 0; j < NT; ++j)
-                        dmma(acc[i][j][0], acc[i][j][1], av, bv[j]);
-                }
+                    dmma(acc[i][j][0], acc[i][j][1], av, bv[j]);
             }
         }
-        __syncwarp();
-        // D tile (i, j) element (rq, 2 kq + v): node 8 i + rq, quantity 8 j + 2 kq + v
+        if (nxt.bin != cur.bin) {
+            // ---- the bin is complete: D tile (i, j) element (rq, 2 kq + u) = node 8 i + rq,
+            //      quantity 8 j + 2 kq + u -> stage -> REDs into the node rows
+            __syncwarp();
 #pragma unroll
-        for (int i = 0; i < L::MT; ++i)
+            for (int i = 0; i < L::MT; ++i)
 #pragma unroll
-            for (int j = 0; j < NT; ++j)
+                for (int j = 0; j < NT; ++j)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    const int a = 8 * i + rq, q = 8 * j + 2 * kq + u;
-                    if (a < L::N && q < NQ)
-                        stage[a * NQ + q] = acc[i][j][u];
-                }
-        const int bxl = (int)(bin / plane), rem = (int)(bin - (int64_t)bxl * plane), bx = g.bx0 + bxl;
-        const int by = rem / g.n2, bz = rem - by * g.n2;
-        if (lane < L::N) {
-            const int a = lane, ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
-                      az = a % (ORDER + 1);
-            rowp[a] = row_ptr(g, g.x_begin + bx - (ORDER - 1) + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2), out,
-                              ghost, NQ);
+                    for (int u = 0; u < 2; ++u) {
+                        const int a = 8 * i + rq, q = 8 * j + 2 * kq + u;
+                        if (a < L::N && q < NQ)
+                            stage[a * NQ + q] = acc[i][j][u];
+                        acc[i][j][u] = 0.0;
+                    }
+            const int bin = (int)cur.bin;
+            const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
+            const int by = rem / g.n2, bz = rem - by * g.n2;
+            if (lane < L::N) {
+                const int a = lane, ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
+                          az = a % (ORDER + 1);
+                rowp[a] = row_ptr(g, g.x_begin + bx - (ORDER - 1) + ax, wrapi(by + ay, g.n1), wrapi(bz + az, g.n2),
+                                  out, ghost, NQ);
+            }
+            __syncwarp();
+            for (int e = lane; e < NE; e += 32)
+                red_add_nc(rowp[e / NQ] + e % NQ, stage[e]);
         }
-        __syncwarp();
-        for (int e = lane; e < NE; e += 32)
-            red_add(rowp[e / NQ] + e % NQ, stage[e]);
-        __syncwarp();
+        cur = nxt;
+        nxt = nxt2;
+        in = nin;
+        nin = nin2;
+        vv = nvv;
     }
 }
 
@@ -168,50 +221,85 @@ __global__ void __launch_bounds__(128) k_gather(Geo g, double *__restrict__ rec,
                                                 const double *__restrict__ F, double *__restrict__ Fp)
 {
     using L = Mo<ORDER>;
-    __shared__ double sF[4][L::N * 3];
+    __shared__ double sF[4][2][L::N * 3];  // the window's nodal field, double-buffered by bin
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int plane = g.n1 * g.n2;
     const int64_t W = (int64_t)gridDim.x * 4;
-    for (int64_t bin = blockIdx.x * 4 + warp; bin < nbins; bin += W) {
-        const int b0 = __ldg(seg_begin + bin), b1 = __ldg(seg_begin + bin + 1);
-        if (b1 == b0)
-            continue;
-        const int bxl = (int)(bin / plane), rem = (int)(bin - (int64_t)bxl * plane), bx = g.bx0 + bxl;
-        const int by = rem / g.n2, bz = rem - by * g.n2;
-        __syncwarp();
-        if (lane < L::N) {  // the window's nodal field (whole periodic domain, global x)
+    // the window's nodal values of a bin (whole periodic domain, global x), one node per lane
+    auto load_f = [&](int64_t bin, double f3[3]) {
+        f3[0] = f3[1] = f3[2] = 0.0;
+        if (bin < nbins && lane < L::N) {
+            const int b = (int)bin, bxl = b / plane, rem = b - bxl * plane, bx = g.bx0 + bxl;
+            const int by = rem / g.n2, bz = rem - by * g.n2;
             const int a = lane, ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
                       az = a % (ORDER + 1);
             int X = g.x_begin + bx - (ORDER - 1) + ax;
             X = X < 0 ? X + g.n0 : (X >= g.n0 ? X - g.n0 : X);
             const double *f = F + 3 * (((int64_t)X * g.n1 + wrapi(by + ay, g.n1)) * g.n2 + wrapi(bz + az, g.n2));
-            sF[warp][3 * a] = __ldg(f), sF[warp][3 * a + 1] = __ldg(f + 1), sF[warp][3 * a + 2] = __ldg(f + 2);
+            f3[0] = __ldg(f), f3[1] = __ldg(f + 1), f3[2] = __ldg(f + 2);
         }
-        __syncwarp();
-        for (int s = b0 + lane; s < b1; s += 32) {
-            const int p = __ldg(perm + s);
-            if (p < 0)
-                continue;  // padding record: its B stays 0
-            double *r = rec + 8 * (int64_t)s;
+    };
+    // two chunks of records + perm in flight (the per-particle work is a few FMAs)
+    auto load_rp = [&](const ChunkIt &c, double4 &r, int &p) {
+        r = make_double4(0, 0, 0, 0);
+        p = -1;
+        if (c.base + lane < c.end) {
+            r = ld256(rec + 8 * (int64_t)(c.base + lane));
+            p = __ldg(perm + c.base + lane);
+        }
+    };
+    ChunkIt cur = first_chunk(blockIdx.x * 4 + warp, W, nbins, seg_begin);
+    ChunkIt nxt = next_chunk(cur, W, nbins, seg_begin);
+    double4 r, nr;
+    int p, np_;
+    load_rp(cur, r, p);
+    load_rp(nxt, nr, np_);
+    double f3[3];
+    load_f(cur.bin, f3);
+    int fb = 0;
+    int64_t fbin = -1;
+    while (cur.bin < nbins) {
+        if (cur.bin != fbin) {  // new bin: its window's field (loaded one bin ahead) into shared memory
+            fb ^= 1;
+            if (lane < L::N)
+                sF[warp][fb][3 * lane] = f3[0], sF[warp][fb][3 * lane + 1] = f3[1], sF[warp][fb][3 * lane + 2] = f3[2];
+            fbin = cur.bin;
+            __syncwarp();
+            // the field of the next bin the stream reaches
+            load_f(first_chunk(cur.bin + W, W, nbins, seg_begin).bin, f3);
+        }
+        const ChunkIt nxt2 = next_chunk(nxt, W, nbins, seg_begin);
+        double4 nr2;
+        int np2;
+        load_rp(nxt2, nr2, np2);
+        if (p >= 0) {
             double wx[3], wy[3], wz[3];
-            axis_weights<ORDER>(r[0], wx);
-            axis_weights<ORDER>(r[1], wy);
-            axis_weights<ORDER>(r[2], wz);
+            axis_weights<ORDER>(r.x, wx);
+            axis_weights<ORDER>(r.y, wy);
+            axis_weights<ORDER>(r.z, wz);
+            const double *sf = sF[warp][fb];
             double b[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int a = 0; a < L::N; ++a) {
                 const int ax = a / ((ORDER + 1) * (ORDER + 1)), ay = (a / (ORDER + 1)) % (ORDER + 1),
                           az = a % (ORDER + 1);
                 const double wa = (wx[ax] * wy[ay]) * wz[az];
-                b[0] = fma(wa, sF[warp][3 * a], b[0]);
-                b[1] = fma(wa, sF[warp][3 * a + 1], b[1]);
-                b[2] = fma(wa, sF[warp][3 * a + 2], b[2]);
+                b[0] = fma(wa, sf[3 * a], b[0]);
+                b[1] = fma(wa, sf[3 * a + 1], b[1]);
+                b[2] = fma(wa, sf[3 * a + 2], b[2]);
             }
-            r[4] = b[0], r[5] = b[1], r[6] = b[2];
+            double *rr = rec + 8 * (int64_t)(cur.base + lane);
+            rr[4] = b[0], rr[5] = b[1], rr[6] = b[2];
             if (Fp) {
                 Fp[3 * (int64_t)p] = b[0], Fp[3 * (int64_t)p + 1] = b[1], Fp[3 * (int64_t)p + 2] = b[2];
             }
         }
+        cur = nxt;
+        nxt = nxt2;
+        r = nr;
+        p = np_;
+        nr = nr2;
+        np_ = np2;
     }
 }
 
