@@ -263,6 +263,8 @@ def main():
     ap.add_argument("--pipeline", action="store_true")
     ap.add_argument("--no-c4", action="store_true")
     ap.add_argument("--no-weak", action="store_true")
+    ap.add_argument("--sync-sort", action="store_true",
+                    help="step with the synchronous mm_sort_by_cell (host round trip) instead of the async sort")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -333,7 +335,11 @@ def main():
         ev = []
 
         def step(record=False):
-            state["h"] = mm.mm_sort_by_cell(grid, order, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"])
+            # mm_sort_by_cell_async: no host round trip between the sort and the assembly; the
+            # deferred domain/finiteness status is checked with mm_sort_wait after the timed loop
+            # (sticky over all steps)
+            state["h"] = mm.mm_sort_by_cell(grid, order, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"],
+                                            wait=args.sync_sort)
             if record:
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
@@ -398,6 +404,7 @@ def main():
             barrier()
         state["h"] = hs[0] if pipeline else state["h"]
         launches = mm.launch_count() - l0
+        mm.mm_sort_wait(state["h"])  # raises if any step met an invalid particle
         ms = t0.elapsed_time(t1)
         if world > 1:
             tt = torch.tensor([ms], device=dev)
@@ -418,6 +425,14 @@ def main():
             s1.record()
             barrier()
             res["sort_ms"] = s0.elapsed_time(s1) / max(5, args.steps // 10)
+            s0.record()
+            for _ in range(max(5, args.steps // 10)):
+                state["h"] = mm.mm_sort_by_cell(grid, order, 4, dd["pos"], dd["q"], dd["B"], handle=state["h"],
+                                                wait=False)
+            s1.record()
+            barrier()
+            mm.mm_sort_wait(state["h"])
+            res["sort_async_ms"] = s0.elapsed_time(s1) / max(5, args.steps // 10)
             # assembly alone (no concurrent sort)
             a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             barrier()
@@ -525,7 +540,9 @@ def main():
             "breakdown": {"pipelined": r1["pipelined"], "sort_alone_ms": r1.get("sort_ms"),
                           "assemble_alone_ms": r1.get("assemble_alone_ms"),
                           "serial_step_ms": (r1.get("sort_ms") or 0) + (r1.get("assemble_alone_ms") or 0),
-                          "sort_ms": r1.get("sort_ms"), "assemble_ms": r1["assemble_ms"],
+                          "sort_ms": r1.get("sort_ms"), "sort_async_ms": r1.get("sort_async_ms"),
+                          "step_sort": "mm_sort_by_cell" if args.sync_sort else "mm_sort_by_cell_async + mm_sort_wait",
+                          "assemble_ms": r1["assemble_ms"],
                           "sort_nearly_sorted_input_ms": sort_nearly_ms,
                           "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
                           # sort against the HBM roofline: algorithmic bytes = 24 B (positions, key
@@ -690,7 +707,8 @@ def main():
             out4 = torch.empty(mm.out_shape(grid4, order, 1), dtype=torch.float64, device=dev)
 
             def sort4():
-                st4["h"] = mm.mm_sort_by_cell(grid4, order, 4, d4["pos"], d4["q"], None, handle=st4["h"])
+                st4["h"] = mm.mm_sort_by_cell(grid4, order, 4, d4["pos"], d4["q"], None, handle=st4["h"],
+                                              wait=args.sync_sort)
 
             def asm4(prec=mm.MM_FP64, o=out4):
                 mm.mm_assemble(st4["h"], mm.MM_SCALAR, prec, sp4, o)
@@ -732,6 +750,7 @@ def main():
                                             "alg_bytes_per_particle": Bf}}
                 del out4f
             c4[name] = ent
+            mm.mm_sort_wait(st4["h"])  # the deferred status of every timed sort
             mm.mm_free(st4["h"])
             del out4
             torch.cuda.empty_cache()
@@ -760,7 +779,8 @@ def main():
             stw = {"h": None}
 
             def sortw():
-                stw["h"] = mm.mm_sort_by_cell(gw, order, 4, dw["pos"], dw["q"], dw["B"], handle=stw["h"])
+                stw["h"] = mm.mm_sort_by_cell(gw, order, 4, dw["pos"], dw["q"], dw["B"], handle=stw["h"],
+                                              wait=args.sync_sort)
 
             def asmw():
                 mm.mm_assemble_slab(stw["h"], 9, mm.MM_FP64, mm.Species(), outw, ghw, comm)
@@ -802,6 +822,7 @@ def main():
                              "frac": aw / fp64_peak, "alg_flops_per_particle": Fw,
                              "note": "mm_assemble_slab (zero-fill, boundary + interior bins, ghost exchange and "
                                      "add), max over ranks"}}
+            mm.mm_sort_wait(stw["h"])
             mm.mm_free(stw["h"])
             del outw, ghw
             torch.cuda.empty_cache()

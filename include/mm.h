@@ -148,6 +148,27 @@ mm_status mm_sort_by_cell(const mm_grid *g, int order, int k_pad, int64_t np, co
 mm_status mm_sort_by_cell_mixed(const mm_grid *g, int order, int k_pad, int64_t np, const float *pos,
                                 const double *q, const float *B, void *stream, mm_sorted **inout);
 
+/*
+ * mm_sort_by_cell_async — mm_sort_by_cell without its host round trip (a PIC step sorts and
+ * assembles back to back on one stream: the host need not wait between them).  Same arguments
+ * and device work; argument checks are synchronous as for mm_sort_by_cell.  The domain /
+ * finiteness checks run on the device into a sticky status word that accumulates over every
+ * sort of the handle until mm_sort_wait reports (and clears) it; np_padded is known only then.
+ * A handle is returned (and created) even if the particles turn out to be invalid: the caller
+ * must call mm_sort_wait before trusting any result computed from it, and frees it with mm_free.
+ */
+mm_status mm_sort_by_cell_async(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos,
+                                const double *q, const double *B, void *stream, mm_sorted **inout);
+
+/*
+ * mm_sort_wait — report the deferred status of the asynchronous sorts of a handle: waits for
+ * `stream` (the sorts' stream, or one ordered after it), returns MM_ERR_DOMAIN /
+ * MM_ERR_NONFINITE if any of them met an invalid particle since the last check (the handle is
+ * then marked invalid), MM_OK otherwise; clears the sticky word.  MM_OK at once if nothing is
+ * pending.  mm_sorted_view waits on the last asynchronous sort's stream by itself.
+ */
+mm_status mm_sort_wait(mm_sorted *h, void *stream);
+
 /* mm_sorted_view — read-only view of a handle's device arrays (see struct). */
 mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
 

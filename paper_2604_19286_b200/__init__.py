@@ -35,7 +35,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
                  4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA", 7: "MM_ERR_NCCL"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
+EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_sort_by_cell_async", "mm_sort_wait", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
            "mm_assemble_slab", "mm_deposit_moments", "mm_gather_field", "mm_apply", "mm_ghost_add", "mm_ghost_exchange", "mm_ghost_planes", "mm_out_elems",
            "mm_comm_unique_id", "mm_comm_create", "mm_comm_free", "mm_free", "mm_last_error", "mm_version",
            "mm_launch_count"]
@@ -82,6 +82,10 @@ def load_library(build_if_missing: bool = True):
     lib.mm_sort_by_cell_mixed.restype = I
     lib.mm_sort_by_cell_mixed.argtypes = [P, I, I, I64, P, P, P, P, P]
     lib.mm_sort_by_cell.restype = I
+    lib.mm_sort_by_cell_async.argtypes = [P, I, I, I64, P, P, P, P, P]
+    lib.mm_sort_by_cell_async.restype = I
+    lib.mm_sort_wait.argtypes = [P, P]
+    lib.mm_sort_wait.restype = I
     lib.mm_sorted_view.argtypes = [P, P]
     lib.mm_sorted_view.restype = I
     lib.mm_assemble.argtypes = [P, I, I, P, I, P, P, P]
@@ -171,9 +175,10 @@ class Sorted:
 
 
 def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handle: Sorted | None = None,
-                    stream=None) -> Sorted:
+                    stream=None, wait: bool = True) -> Sorted:
     """Stable support-window binning with K-padding (include/mm.h).  Reuses `handle` if given.
-    FP32 pos (and B) select mm_sort_by_cell_mixed (PAPER.md:572 storage; q stays FP64)."""
+    FP32 pos (and B) select mm_sort_by_cell_mixed (PAPER.md:572 storage; q stays FP64).
+    wait=False: mm_sort_by_cell_async (no host round trip; check with mm_sort_wait)."""
     lib = load_library()
     f32 = pos is not None and pos.dtype == torch.float32
     np_ = int(pos.shape[0]) if pos is not None else 0
@@ -185,7 +190,9 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
         raise MMError(MM_ERR_INVALID_ARG, "handle was freed")
     hp = ctypes.c_void_p(handle.ptr.value if handle is not None else None)
     pdt = torch.float32 if f32 else torch.float64
-    fn = lib.mm_sort_by_cell_mixed if f32 else lib.mm_sort_by_cell
+    if not wait and f32:
+        raise MMError(MM_ERR_INVALID_ARG, "the asynchronous sort takes FP64 positions")
+    fn = lib.mm_sort_by_cell_mixed if f32 else (lib.mm_sort_by_cell if wait else lib.mm_sort_by_cell_async)
     st = fn(ctypes.byref(grid), int(order), int(k_pad), np_,
             _dev_ptr(pos, pdt, name="pos") if np_ else None, _dev_ptr(q, name="q") if np_ else None,
             _dev_ptr(B, pdt, name="B") if (B is not None and np_) else None, _stream_ptr(stream),
@@ -195,6 +202,11 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
         handle._ptr = hp  # the library may only grow buffers in place; keep the pointer it returned
         return handle
     return Sorted(hp, grid, order)
+
+
+def mm_sort_wait(handle: Sorted, stream=None):
+    """Deferred status of the asynchronous sorts of `handle` (include/mm.h); raises MMError."""
+    _check(load_library().mm_sort_wait(handle.ptr, _stream_ptr(stream)))
 
 
 class _CudaArray:

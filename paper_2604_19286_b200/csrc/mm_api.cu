@@ -36,6 +36,11 @@ struct mm_sorted {
     int32_t *h_status;  // pinned
     int32_t *d_work;    // assembly work counter
     int32_t *d_flags;   // first-writer zeroing: one flag per output node row (lazily allocated)
+    int pending;        // an asynchronous sort whose status has not been checked (mm_sort_wait)
+    int64_t bkt_cap;    // capacity the bucketed-scatter buffers were sized for (0: none)
+    int2 *bkt_pairs;
+    int32_t *bkt_count, *bkt_off, *bkt_scan, *bkt_misc;
+    void *sort_stream;  // the stream of the last asynchronous sort
     int32_t epoch;      // flag value of the last zeroing launch
 };
 
@@ -101,6 +106,11 @@ void release(mm_sorted *h)
     cudaFree(h->d_status);
     cudaFree(h->d_work);
     cudaFree(h->d_flags);
+    cudaFree(h->bkt_pairs);
+    cudaFree(h->bkt_count);
+    cudaFree(h->bkt_off);
+    cudaFree(h->bkt_scan);
+    cudaFree(h->bkt_misc);
     if (h->h_status)
         cudaFreeHost(h->h_status);
     delete h;
@@ -178,7 +188,7 @@ int64_t mm_out_elems(const mm_grid *g, int order, mm_kind kind)
 namespace {
 // pos / B point to FP64 arrays (f32 = 0) or FP32 arrays (f32 = 1, widened exactly on load)
 mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const void *pos, const double *q,
-                      const void *B, int f32, void *stream, mm_sorted **inout)
+                      const void *B, int f32, void *stream, mm_sorted **inout, bool async = false)
 {
     try {
         mm_status st = check_grid(g, order);
@@ -245,6 +255,26 @@ mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const 
             if (!e) e = cudaMalloc((void **)&h->d_status, sizeof(int32_t) * mm::ST_WORDS);
             if (!e) e = cudaMalloc((void **)&h->d_work, sizeof(int32_t) * 4);
             if (!e) e = cudaMallocHost((void **)&h->h_status, sizeof(int32_t) * mm::ST_WORDS);
+            if (!e) e = cudaMemsetAsync(h->d_status, 0, sizeof(int32_t) * mm::ST_WORDS, (cudaStream_t)stream);
+        }
+        // bucketed scatter buffers for inputs beyond L2 (sort)
+        const bool bkt = np >= mm::bkt_min_np();
+        if (!e && bkt && h->bkt_cap < h->cap_rec) {
+            cudaFree(h->bkt_pairs);
+            cudaFree(h->bkt_count);
+            cudaFree(h->bkt_off);
+            cudaFree(h->bkt_scan);
+            cudaFree(h->bkt_misc);
+            h->bkt_pairs = nullptr;
+            h->bkt_count = h->bkt_off = h->bkt_scan = h->bkt_misc = nullptr;
+            h->bkt_cap = 0;
+            const int64_t ne = mm::bkt_elems(h->cap_rec);
+            e = cudaMalloc((void **)&h->bkt_pairs, sizeof(int2) * (size_t)h->cap_rec);
+            if (!e) e = cudaMalloc((void **)&h->bkt_count, sizeof(int32_t) * (size_t)ne);
+            if (!e) e = cudaMalloc((void **)&h->bkt_off, sizeof(int32_t) * (size_t)ne);
+            if (!e) e = cudaMalloc((void **)&h->bkt_scan, sizeof(int32_t) * (size_t)mm::scan_tmp_elems(ne));
+            if (!e) e = cudaMalloc((void **)&h->bkt_misc, sizeof(int32_t) * (mm::ST_WORDS + 1));
+            if (!e) h->bkt_cap = h->cap_rec;
         }
         if (e) {
             if (fresh)
@@ -275,9 +305,30 @@ mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const 
         b.huge_list = h->huge_list;
         b.status = h->d_status;
         b.capacity = h->cap_rec;
+        b.bkt_pairs = bkt ? h->bkt_pairs : nullptr;
+        b.bkt_count = h->bkt_count;
+        b.bkt_off = h->bkt_off;
+        b.bkt_scan = h->bkt_scan;
+        b.bkt_misc = h->bkt_misc;
         e = mm::sort_enqueue(mm::make_geo(*g, order), b, s);
+        if (async) {
+            // no host round trip: the status stays on the device (sticky error word) until
+            // mm_sort_wait; np_padded is read there too
+            if (e) {
+                if (fresh)
+                    release(h);
+                return cuda_fail(e, "mm_sort_by_cell_async");
+            }
+            h->valid = 1;
+            h->pending = 1;
+            h->sort_stream = stream;
+            *inout = h;
+            return MM_OK;
+        }
         if (!e)
             e = cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int32_t) * mm::ST_WORDS, cudaMemcpyDeviceToHost, s);
+        if (!e)  // this sort's errors are reported now: clear the sticky word
+            e = cudaMemsetAsync(h->d_status + mm::ST_STICKY, 0, sizeof(int32_t), s);
         if (!e)
             e = cudaStreamSynchronize(s);
         if (e) {
@@ -317,10 +368,52 @@ mm_status mm_sort_by_cell_mixed(const mm_grid *g, int order, int k_pad, int64_t 
     return sort_common(g, order, k_pad, np, pos, q, B, 1, stream, inout);
 }
 
+mm_status mm_sort_by_cell_async(const mm_grid *g, int order, int k_pad, int64_t np, const double *pos,
+                                const double *q, const double *B, void *stream, mm_sorted **inout)
+{
+    return sort_common(g, order, k_pad, np, pos, q, B, 0, stream, inout, true);
+}
+
+mm_status mm_sort_wait(mm_sorted *h, void *stream)
+{
+    try {
+        if (!h)
+            return fail(MM_ERR_INVALID_ARG, "NULL handle");
+        if (!h->pending)
+            return MM_OK;
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaError_t e = cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int32_t) * mm::ST_WORDS,
+                                        cudaMemcpyDeviceToHost, s);
+        if (!e)
+            e = cudaMemsetAsync(h->d_status + mm::ST_STICKY, 0, sizeof(int32_t), s);
+        if (!e)
+            e = cudaStreamSynchronize(s);
+        if (e)
+            return cuda_fail(e, "mm_sort_wait");
+        h->pending = 0;
+        h->np_padded = h->h_status[mm::ST_NPAD];
+        const int err = h->h_status[mm::ST_STICKY];
+        if (err) {
+            h->valid = 0;
+            if (err & mm::ERR_NONFINITE)
+                return fail(MM_ERR_NONFINITE, "NaN/Inf in particle positions, charges or B (asynchronous sort)");
+            return fail(MM_ERR_DOMAIN, "particle outside the owned cell slab (asynchronous sort)");
+        }
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_sort_wait");
+    }
+}
+
 mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out)
 {
     if (!h || !out)
         return fail(MM_ERR_INVALID_ARG, "NULL argument");
+    if (h->pending) {
+        mm_status st = mm_sort_wait(const_cast<mm_sorted *>(h), h->sort_stream);
+        if (st)
+            return st;
+    }
     if (!h->valid)
         return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort");
     out->np = h->np;
