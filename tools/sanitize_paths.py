@@ -22,9 +22,9 @@ def main(which="small"):
     else:
         n, ppc = (12, 10, 9), 40
     sp = mm.Species()
-    for order in (1, 2):
+    for order in ((1,) if which == "c1" else (1, 2)):  # c1 (4^3) admits order 1 only (n >= 2 order + 1)
         for slab in (False, True):
-            xb, xe = (0, n[0]) if not slab else (3, 3 + 2 * order + 2)
+            xb, xe = (0, n[0]) if not slab else ((1, 3) if which == "c1" else (3, 3 + 2 * order + 2))
             cfg = synth.Config("san", n, order, "tensor", ppc, seed=7 + order)
             d = synth.particles(cfg, x_begin=xb, x_end=xe)
             dd = {k: torch.from_numpy(v).cuda() for k, v in d.items()}
