@@ -37,9 +37,6 @@ struct mm_sorted {
     int32_t *d_work;    // assembly work counter
     int32_t *d_flags;   // first-writer zeroing: one flag per output node row (lazily allocated)
     int pending;        // an asynchronous sort whose status has not been checked (mm_sort_wait)
-    int64_t bkt_cap;    // capacity the bucketed-scatter buffers were sized for (0: none)
-    int2 *bkt_pairs;
-    int32_t *bkt_count, *bkt_off, *bkt_scan, *bkt_misc;
     void *sort_stream;  // the stream of the last asynchronous sort
     int32_t epoch;      // flag value of the last zeroing launch
 };
@@ -106,11 +103,6 @@ void release(mm_sorted *h)
     cudaFree(h->d_status);
     cudaFree(h->d_work);
     cudaFree(h->d_flags);
-    cudaFree(h->bkt_pairs);
-    cudaFree(h->bkt_count);
-    cudaFree(h->bkt_off);
-    cudaFree(h->bkt_scan);
-    cudaFree(h->bkt_misc);
     if (h->h_status)
         cudaFreeHost(h->h_status);
     delete h;
@@ -257,25 +249,6 @@ mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const 
             if (!e) e = cudaMallocHost((void **)&h->h_status, sizeof(int32_t) * mm::ST_WORDS);
             if (!e) e = cudaMemsetAsync(h->d_status, 0, sizeof(int32_t) * mm::ST_WORDS, (cudaStream_t)stream);
         }
-        // bucketed scatter buffers for inputs beyond L2 (sort)
-        const bool bkt = np >= mm::bkt_min_np();
-        if (!e && bkt && h->bkt_cap < h->cap_rec) {
-            cudaFree(h->bkt_pairs);
-            cudaFree(h->bkt_count);
-            cudaFree(h->bkt_off);
-            cudaFree(h->bkt_scan);
-            cudaFree(h->bkt_misc);
-            h->bkt_pairs = nullptr;
-            h->bkt_count = h->bkt_off = h->bkt_scan = h->bkt_misc = nullptr;
-            h->bkt_cap = 0;
-            const int64_t ne = mm::bkt_elems(h->cap_rec);
-            e = cudaMalloc((void **)&h->bkt_pairs, sizeof(int2) * (size_t)h->cap_rec);
-            if (!e) e = cudaMalloc((void **)&h->bkt_count, sizeof(int32_t) * (size_t)ne);
-            if (!e) e = cudaMalloc((void **)&h->bkt_off, sizeof(int32_t) * (size_t)ne);
-            if (!e) e = cudaMalloc((void **)&h->bkt_scan, sizeof(int32_t) * (size_t)mm::scan_tmp_elems(ne));
-            if (!e) e = cudaMalloc((void **)&h->bkt_misc, sizeof(int32_t) * (mm::ST_WORDS + 1));
-            if (!e) h->bkt_cap = h->cap_rec;
-        }
         if (e) {
             if (fresh)
                 release(h);
@@ -305,11 +278,6 @@ mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const 
         b.huge_list = h->huge_list;
         b.status = h->d_status;
         b.capacity = h->cap_rec;
-        b.bkt_pairs = bkt ? h->bkt_pairs : nullptr;
-        b.bkt_count = h->bkt_count;
-        b.bkt_off = h->bkt_off;
-        b.bkt_scan = h->bkt_scan;
-        b.bkt_misc = h->bkt_misc;
         e = mm::sort_enqueue(mm::make_geo(*g, order), b, s);
         if (async) {
             // no host round trip: the status stays on the device (sticky error word) until

@@ -62,17 +62,7 @@ struct SortBufs {
     int32_t *huge_list;  // [nbins]
     int32_t *status;     // [ST_WORDS]
     int64_t capacity;
-    // bucketed scatter for inputs beyond L2 (bkt_pairs == nullptr: direct random writes)
-    int2 *bkt_pairs;     // [capacity]
-    int32_t *bkt_count;  // [bkt_elems(capacity)] per (bucket, tile) counts, then their exclusive scan
-    int32_t *bkt_off;    // [bkt_elems(capacity)]
-    int32_t *bkt_scan;   // [scan_tmp_elems(bkt_elems(capacity))]
-    int32_t *bkt_misc;   // [ST_WORDS + 1]: scan total / scratch status
 };
-// (bucket, tile) counters of the bucketed scatter for outputs of `cap` elements
-int64_t bkt_elems(int64_t cap);
-// inputs from this many particles on take the bucketed scatter (MM_SORT_BKT_MIN overrides)
-int64_t bkt_min_np();
 int64_t scan_tmp_elems(int64_t nbins);
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s);
 

@@ -288,8 +288,10 @@ __global__ void __launch_bounds__(128) k_gather(Geo g, double *__restrict__ rec,
                 b[1] = fma(wa, sf[3 * a + 1], b[1]);
                 b[2] = fma(wa, sf[3 * a + 2], b[2]);
             }
-            double *rr = rec + 8 * (int64_t)(cur.base + lane);
-            rr[4] = b[0], rr[5] = b[1], rr[6] = b[2];
+            // the record's second sector {B, 0} as ONE full 32-B store (no partial-sector write)
+            double *rr = rec + 8 * (int64_t)(cur.base + lane) + 4;
+            asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rr), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(0.0)
+                         : "memory");
             if (Fp) {
                 Fp[3 * (int64_t)p] = b[0], Fp[3 * (int64_t)p + 1] = b[1], Fp[3 * (int64_t)p + 2] = b[2];
             }

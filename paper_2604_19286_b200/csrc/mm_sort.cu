@@ -687,96 +687,6 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP 
     }
 }
 
-// ---- bucketed scatter of int32 pairs (inputs beyond L2) --------------------------------
-// The two random 4-B write passes of the sort - perm[seg_begin[key] + rank] = p (place) and
-// dest[perm[s]] = s (the inverse permutation, for the record scatter) - cost one DRAM sector
-// read-modify-write per 4-B store once the arrays (4 B x np) outgrow the L2.  For large inputs
-// they go through a bucket pass instead: count (idx >> BKT_SHIFT) per tile, exclusive scan in
-// (bucket, tile) order, distribute the (idx, val) pairs into their buckets (a few hundred
-// write streams per tile, merged in L2), then apply each bucket's pairs into its 4 MB slice of
-// the output, which stays in L2 until it is written back once.
-constexpr int BKT_SHIFT = 20, BKT_TILE = 16384, BKT_T = 512;
-
-// MODE 0 (place): element i = particle p: idx = seg_begin[key[p]] + rank[p], val = p
-// MODE 1 (inverse): element i = slot s: idx = perm[s] (padding -1: none), val = s
-template <int MODE>
-__device__ __forceinline__ bool bkt_elem(int64_t i, const uint32_t *__restrict__ key,
-                                         const int32_t *__restrict__ rank, const int32_t *__restrict__ seg_begin,
-                                         const int32_t *__restrict__ perm, int32_t &idx, int32_t &val)
-{
-    if (MODE == 0) {
-        const uint32_t k = key[i];
-        if (k == 0xffffffffu)
-            return false;
-        idx = __ldg(seg_begin + k) + rank[i];
-    } else {
-        idx = perm[i];
-        if (idx < 0)
-            return false;
-    }
-    val = (int32_t)i;
-    return true;
-}
-
-// n: element count (MODE 1: read from *n_dev, the padded total of the scan)
-template <int MODE>
-__global__ void __launch_bounds__(BKT_T) k_bkt_count(int64_t n, const int32_t *__restrict__ n_dev,
-                                                     const uint32_t *__restrict__ key,
-                                                     const int32_t *__restrict__ rank,
-                                                     const int32_t *__restrict__ seg_begin,
-                                                     const int32_t *__restrict__ perm, int nb, int ntiles,
-                                                     int32_t *__restrict__ bcount)
-{
-    extern __shared__ int32_t h[];
-    if (n_dev)
-        n = *n_dev;
-    for (int b = threadIdx.x; b < nb; b += BKT_T)
-        h[b] = 0;
-    __syncthreads();
-    const int64_t i0 = (int64_t)blockIdx.x * BKT_TILE, i1 = min(n, i0 + BKT_TILE);
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += BKT_T) {
-        int32_t idx, val;
-        if (bkt_elem<MODE>(i, key, rank, seg_begin, perm, idx, val))
-            atomicAdd(&h[idx >> BKT_SHIFT], 1);
-    }
-    __syncthreads();
-    for (int b = threadIdx.x; b < nb; b += BKT_T)
-        bcount[(int64_t)b * ntiles + blockIdx.x] = h[b];
-}
-
-template <int MODE>
-__global__ void __launch_bounds__(BKT_T) k_bkt_distribute(int64_t n, const int32_t *__restrict__ n_dev,
-                                                          const uint32_t *__restrict__ key,
-                                                          const int32_t *__restrict__ rank,
-                                                          const int32_t *__restrict__ seg_begin,
-                                                          const int32_t *__restrict__ perm, int nb, int ntiles,
-                                                          const int32_t *__restrict__ boff, int2 *__restrict__ pairs)
-{
-    extern __shared__ int32_t cur[];
-    if (n_dev)
-        n = *n_dev;
-    for (int b = threadIdx.x; b < nb; b += BKT_T)
-        cur[b] = boff[(int64_t)b * ntiles + blockIdx.x];
-    __syncthreads();
-    const int64_t i0 = (int64_t)blockIdx.x * BKT_TILE, i1 = min(n, i0 + BKT_TILE);
-    for (int64_t i = i0 + threadIdx.x; i < i1; i += BKT_T) {
-        int32_t idx, val;
-        if (bkt_elem<MODE>(i, key, rank, seg_begin, perm, idx, val))
-            pairs[atomicAdd(&cur[idx >> BKT_SHIFT], 1)] = make_int2(idx, val);
-    }
-}
-
-// pairs in bucket order: consecutive CTAs work in the same few output slices
-__global__ void __launch_bounds__(256) k_bkt_apply(const int32_t *__restrict__ total, const int2 *__restrict__ pairs,
-                                                   int32_t *__restrict__ out)
-{
-    const int64_t m = *total;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
-        const int2 pr = pairs[i];
-        out[pr.x] = pr.y;
-    }
-}
-
 inline unsigned blocks_for(int64_t n, int t)
 {
     return (unsigned)((n + t - 1) / t);
@@ -830,47 +740,6 @@ int64_t scan_tmp_elems(int64_t nbins)
     return (nbins + SCAN_TILE - 1) / SCAN_TILE + 1;
 }
 
-int64_t bkt_elems(int64_t cap)
-{
-    const int64_t nb = (cap + (1 << BKT_SHIFT) - 1) >> BKT_SHIFT, nt = (cap + BKT_TILE - 1) / BKT_TILE;
-    return nb * nt + 1;
-}
-
-int64_t bkt_min_np()
-{
-    static const int64_t v = [] {
-        const char *e = getenv("MM_SORT_BKT_MIN");
-        return e ? (int64_t)atoll(e) : (int64_t)24 * 1000 * 1000;
-    }();
-    return v;
-}
-
-namespace {
-// out[idx] = val for the pairs of MODE (see bkt_elem) through the bucket pass.  n elements
-// (n_dev != nullptr: the device-side count), outputs of n_out elements.
-template <int MODE>
-cudaError_t bkt_scatter(const SortBufs &b, int64_t n, const int32_t *n_dev, int64_t n_out, int32_t *out,
-                        cudaStream_t s)
-{
-    const int nb = (int)((n_out + (1 << BKT_SHIFT) - 1) >> BKT_SHIFT);
-    const int ntiles = (int)((n + BKT_TILE - 1) / BKT_TILE);
-    if (ntiles == 0 || nb == 0)
-        return cudaSuccess;
-    const int64_t N = (int64_t)nb * ntiles;
-    const size_t sm = (size_t)nb * 4;
-    k_bkt_count<MODE><<<ntiles, BKT_T, sm, s>>>(n, n_dev, b.key, b.rank, b.seg_begin, b.perm, nb, ntiles, b.bkt_count);
-    const int nblk = (int)((N + SCAN_TILE - 1) / SCAN_TILE);
-    k_scan_local<<<nblk, SCAN_T, 0, s>>>(b.bkt_count, N, 1, b.bkt_off, b.bkt_scan);
-    k_scan_top<<<1, SCAN_T, 0, s>>>(b.bkt_scan, nblk, b.bkt_misc, b.bkt_misc + 1);
-    k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.bkt_off, N, b.bkt_scan);
-    k_bkt_distribute<MODE><<<ntiles, BKT_T, sm, s>>>(n, n_dev, b.key, b.rank, b.seg_begin, b.perm, nb, ntiles,
-                                                     b.bkt_off, b.bkt_pairs);
-    k_bkt_apply<<<148 * 8, 256, 0, s>>>(b.bkt_misc, b.bkt_pairs, out);
-    count_launch(6);
-    return cudaGetLastError();
-}
-}  // namespace
-
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
 {
     cudaError_t e;
@@ -898,20 +767,12 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
     count_launch(3);
     pt.mark("scan");
-    const bool bkt = b.bkt_pairs != nullptr;
     if (b.np > 0) {
-        if (bkt) {
-            if ((e = bkt_scatter<0>(b, b.np, nullptr, b.capacity, b.perm, s)))
-                return e;
-        } else {
-            k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
-            count_launch();
-        }
+        k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
+        count_launch();
         pt.mark("place");
     }
-    // with the bucketed path the fix-ups leave dest alone; the inverse permutation is one
-    // bucketed pass over the sorted slots afterwards
-    int32_t *dest = bkt ? nullptr : b.rank;
+    int32_t *dest = b.rank;
     {
         int64_t want = (b.nbins + FIX_WARPS - 1) / FIX_WARPS;
         unsigned grid = (unsigned)(want < 148 * 16 ? want : 148 * 16);
@@ -934,12 +795,7 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         k_fix_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.seg_begin, b.perm, dest, b.huge_list, b.status);
         count_launch();
     }
-    if (bkt && b.np > 0) {
-        // dest[perm[s]] = s over the padded slots [0, np_padded) (the scan's total, on the device)
-        if ((e = bkt_scatter<1>(b, b.capacity, b.status + ST_NPAD, b.np, b.rank, s)))
-            return e;
-        pt.mark("inverse");
-    }
+
     if (b.np > 0) {
         const unsigned gs = blocks_for((b.np + 3) / 4, T);
         constexpr int SCAT_SMEM = 256 * 4 * 64;
