@@ -93,7 +93,7 @@ __device__ __forceinline__ MoIn load_mo(const ChunkIt &c, int lane, const double
 }
 
 template <int ORDER, int NQ>
-__global__ void __launch_bounds__(128) k_moments(Geo g, const double *__restrict__ rec, int rs,
+__global__ void __launch_bounds__(128, ORDER == 1 ? 6 : 4) k_moments(Geo g, const double *__restrict__ rec, int rs,
                                                  const int32_t *__restrict__ perm,
                                                  const int32_t *__restrict__ seg_begin, int64_t nbins,
                                                  const double *__restrict__ v, double sigma,
@@ -118,11 +118,21 @@ __global__ void __launch_bounds__(128) k_moments(Geo g, const double *__restrict
     const int64_t W = (int64_t)gridDim.x * 4;
     // three-stage pipeline over the warp's chunks: records + perm two chunks ahead, the
     // velocities (random reads through perm) one chunk ahead
+    const bool v16 = ((uintptr_t)v & 15) == 0;
     auto load_v = [&](const MoIn &x) {
         double3 r3 = make_double3(0, 0, 0);
-        if (x.p >= 0)
-            r3 = make_double3(__ldg(v + 3 * (int64_t)x.p), __ldg(v + 3 * (int64_t)x.p + 1),
-                              __ldg(v + 3 * (int64_t)x.p + 2));
+        if (x.p >= 0) {
+            const double *a = v + 3 * (int64_t)x.p;
+            if (v16 && (x.p & 1) == 0) {  // 24 B at a random place: two requests instead of three
+                const double2 u = __ldg(reinterpret_cast<const double2 *>(a));
+                r3 = make_double3(u.x, u.y, __ldg(a + 2));
+            } else if (v16) {
+                const double2 u = __ldg(reinterpret_cast<const double2 *>(a + 1));
+                r3 = make_double3(__ldg(a), u.x, u.y);
+            } else {
+                r3 = make_double3(__ldg(a), __ldg(a + 1), __ldg(a + 2));
+            }
+        }
         return r3;
     };
     ChunkIt cur = first_chunk(blockIdx.x * 4 + warp, W, nbins, seg_begin);
@@ -248,6 +258,7 @@ __global__ void __launch_bounds__(128) k_gather(Geo g, double *__restrict__ rec,
             p = __ldg(perm + c.base + lane);
         }
     };
+    const bool fp16 = ((uintptr_t)Fp & 15) == 0;
     ChunkIt cur = first_chunk(blockIdx.x * 4 + warp, W, nbins, seg_begin);
     ChunkIt nxt = next_chunk(cur, W, nbins, seg_begin);
     double4 r, nr;
@@ -293,7 +304,19 @@ __global__ void __launch_bounds__(128) k_gather(Geo g, double *__restrict__ rec,
             asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(rr), "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(0.0)
                          : "memory");
             if (Fp) {
-                Fp[3 * (int64_t)p] = b[0], Fp[3 * (int64_t)p + 1] = b[1], Fp[3 * (int64_t)p + 2] = b[2];
+                // 24 B at a random place: two requests (16-B aligned pair + single) instead of three
+                double *f = Fp + 3 * (int64_t)p;
+                if (fp16) {
+                    if ((p & 1) == 0) {
+                        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(f), "d"(b[0]), "d"(b[1]) : "memory");
+                        f[2] = b[2];
+                    } else {
+                        f[0] = b[0];
+                        asm volatile("st.global.v2.f64 [%0], {%1,%2};" ::"l"(f + 1), "d"(b[1]), "d"(b[2]) : "memory");
+                    }
+                } else {
+                    f[0] = b[0], f[1] = b[1], f[2] = b[2];
+                }
             }
         }
         cur = nxt;
