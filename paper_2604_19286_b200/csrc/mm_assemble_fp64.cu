@@ -405,6 +405,9 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
     const int kq = lane & 3, rq = lane >> 2;
     const double *xa = xz + rq * L::XS + kq;
     const double *zb = xz + (8 * L::MT + rq) * L::XS + kq;
+    // bin coordinates stepped by the mixed-radix digits of nw (no integer division per bin)
+    const int wz = nw % g.n2, wy = (nw / g.n2) % g.n1, wx = nw / plane;
+    int cx = bin / plane, cy = (bin - cx * plane) / g.n2, cz = bin - cx * plane - cy * g.n2;
     while (bin < nbins) {
         int nn0 = 0, nn1 = 0;
         if (bin + 2 * nw < nbins) {
@@ -493,8 +496,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                     if (x < L::NX && z < L::NZ)
                         stage[x * L::NZ + z] = acc[mt][v];
                 }
-            const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
-            const int by = rem / g.n2, bz = rem - by * g.n2;
+            const int bx = g.bx0 + cx, by = cy, bz = cz;
             if (lane < L::NA) {
                 const int a = lane;
                 const int ax = ORDER == 1 ? a >> 2 : a / 9, ay = ORDER == 1 ? (a >> 1) & 1 : (a / 3) % 3,
@@ -515,6 +517,17 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
             ra = ld256(rec + rs * (int64_t)(nb0 + lane));
         }
         bin += nw;
+        cz += wz;
+        if (cz >= g.n2) {
+            cz -= g.n2;
+            ++cy;
+        }
+        cy += wy;
+        if (cy >= g.n1) {
+            cy -= g.n1;
+            ++cx;
+        }
+        cx += wx;
         b0 = nb0;
         b1 = nb1;
         nb0 = nn0;

@@ -110,6 +110,20 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
         cur = __shfl_sync(0xffffffffu, cur, 0);
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
     }
+    // bin coordinates (bin plane x, y, z) of the static schedule, stepped by the mixed-radix
+    // digits of W instead of two integer divisions per bin
+    int cx = 0, cy = 0, cz = 0, wx = 0, wy = 0, wz = 0;
+    if (!ZERO) {
+        wz = W % g.n2;
+        wy = (W / g.n2) % g.n1;
+        wx = W / plane;
+        if (cur < nbins) {
+            const int bin = nbins - 1 - cur;
+            cx = bin / plane;
+            cy = (bin - cx * plane) / g.n2;
+            cz = bin - cx * plane - cy * g.n2;
+        }
+    }
     int64_t rel = -1;  // flag index of a row this lane publishes before the warp's next wait
     auto zero_task = [&](int tk, int lbase) {
         if (tk + zp.lookahead < nbins)
@@ -143,8 +157,14 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
         if (ZERO && lane == 0)
             nn = ticket(work);  // consumed at the end of this bin
         const int bin = nbins - 1 - cur;
-        const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
-        const int by = rem / g.n2, bz = rem - by * g.n2;
+        int bxl = cx, by = cy, bz = cz;
+        if (ZERO) {
+            bxl = bin / plane;
+            const int rem = bin - bxl * plane;
+            by = rem / g.n2;
+            bz = rem - by * g.n2;
+        }
+        const int bx = g.bx0 + bxl;
         if (b1 > b0) {
             double acc[5][2], acc8[3];
 #pragma unroll
@@ -284,6 +304,19 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
         }  // rel is free: released above (or still pending for an empty bin)
         cur = nxt;
         nxt = nn;
+        if (!ZERO) {  // bin - W
+            cz -= wz;
+            if (cz < 0) {
+                cz += g.n2;
+                --cy;
+            }
+            cy -= wy;
+            if (cy < 0) {
+                cy += g.n1;
+                --cx;
+            }
+            cx -= wx;
+        }
         b0 = nb0;
         b1 = nb1;
         if (nxt < nbins) {
