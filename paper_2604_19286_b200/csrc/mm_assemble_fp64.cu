@@ -570,6 +570,7 @@ inline int cta_cap()
 
 cudaError_t launch_o2t(const Geo &geo, const AsmArgs &a, cudaStream_t s)
 {
+
     using L = O2T;
     // per call: the attribute is per device/context (a process may drive several GPUs)
     cudaError_t e = cudaFuncSetAttribute(k_asm_o2t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::SMEM);
