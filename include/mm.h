@@ -169,6 +169,22 @@ mm_status mm_sort_by_cell_async(const mm_grid *g, int order, int k_pad, int64_t 
  */
 mm_status mm_sort_wait(mm_sorted *h, void *stream);
 
+/*
+ * mm_resort_by_cell — incremental re-binning of the SAME particles after they moved (SURVEY.md
+ * NEXT-1, the "sort & communicate" stage of a PIC cycle).  The handle must
+ * hold a valid sort of np particles in the same order (same grid, order, k_pad; B given iff it
+ * was).  Every particle is re-keyed; only those whose support-window bin changed update the bin
+ * counters; each bin's new member list is its old stable slice minus the leavers plus its
+ * arrivals, put back in ascending particle order; the records are rewritten from the new
+ * positions.  The result (perm, seg_begin, records) is bit-identical to mm_sort_by_cell of the
+ * new positions.  wait = 1: errors reported synchronously as by mm_sort_by_cell (the handle is
+ * then invalid); wait = 0: deferred as by mm_sort_by_cell_async (mm_sort_wait).  Errors:
+ * MM_ERR_INCOMPATIBLE (no valid previous sort, np or B presence differ), MM_ERR_DOMAIN,
+ * MM_ERR_NONFINITE, MM_ERR_CUDA.
+ */
+mm_status mm_resort_by_cell(mm_sorted *h, int64_t np, const double *pos, const double *q, const double *B,
+                            void *stream, int wait);
+
 /* mm_sorted_view — read-only view of a handle's device arrays (see struct). */
 mm_status mm_sorted_view(const mm_sorted *h, mm_sorted_info *out);
 

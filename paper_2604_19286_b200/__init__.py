@@ -35,7 +35,7 @@ _STATUS_NAMES = {0: "MM_OK", 1: "MM_ERR_INVALID_ARG", 2: "MM_ERR_DOMAIN", 3: "MM
                  4: "MM_ERR_INCOMPATIBLE", 5: "MM_ERR_OUT_OF_MEMORY", 6: "MM_ERR_CUDA", 7: "MM_ERR_NCCL"}
 
 # Every symbol include/mm.h declares (checked by the CPU test suite).
-EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_sort_by_cell_async", "mm_sort_wait", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
+EXPORTS = ["mm_sort_by_cell", "mm_sort_by_cell_mixed", "mm_sort_by_cell_async", "mm_sort_wait", "mm_resort_by_cell", "mm_slab_partition", "mm_sorted_view", "mm_assemble",
            "mm_assemble_slab", "mm_deposit_moments", "mm_gather_field", "mm_apply", "mm_ghost_add", "mm_ghost_exchange", "mm_ghost_planes", "mm_out_elems",
            "mm_comm_unique_id", "mm_comm_create", "mm_comm_free", "mm_free", "mm_last_error", "mm_version",
            "mm_launch_count"]
@@ -84,6 +84,8 @@ def load_library(build_if_missing: bool = True):
     lib.mm_sort_by_cell.restype = I
     lib.mm_sort_by_cell_async.argtypes = [P, I, I, I64, P, P, P, P, P]
     lib.mm_sort_by_cell_async.restype = I
+    lib.mm_resort_by_cell.argtypes = [P, I64, P, P, P, P, I]
+    lib.mm_resort_by_cell.restype = I
     lib.mm_sort_wait.argtypes = [P, P]
     lib.mm_sort_wait.restype = I
     lib.mm_sorted_view.argtypes = [P, P]
@@ -202,6 +204,18 @@ def mm_sort_by_cell(grid: mm_grid, order: int, k_pad: int, pos, q, B=None, handl
         handle._ptr = hp  # the library may only grow buffers in place; keep the pointer it returned
         return handle
     return Sorted(hp, grid, order)
+
+
+def mm_resort_by_cell(handle: Sorted, pos, q, B=None, stream=None, wait: bool = True) -> Sorted:
+    """Incremental re-binning of the same particles after they moved (include/mm.h); FP64 inputs."""
+    np_ = int(pos.shape[0])
+    if tuple(pos.shape) != (np_, 3) or (B is not None and tuple(B.shape) != (np_, 3)):
+        raise MMError(MM_ERR_INVALID_ARG, "pos / B must be [np, 3]")
+    _check(load_library().mm_resort_by_cell(handle.ptr, np_, _dev_ptr(pos, name="pos") if np_ else None,
+                                            _dev_ptr(q, name="q") if np_ else None,
+                                            _dev_ptr(B, name="B") if (B is not None and np_) else None,
+                                            _stream_ptr(stream), int(bool(wait))))
+    return handle
 
 
 def mm_sort_wait(handle: Sorted, stream=None):

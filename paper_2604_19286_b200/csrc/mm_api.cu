@@ -38,6 +38,10 @@ struct mm_sorted {
     int32_t *d_flags;   // first-writer zeroing: one flag per output node row (lazily allocated)
     int pending;        // an asynchronous sort whose status has not been checked (mm_sort_wait)
     void *sort_stream;  // the stream of the last asynchronous sort
+    // incremental re-binning (mm_resort_by_cell), lazily allocated
+    int32_t *perm2;     // [cap_rec] the other permutation buffer
+    int32_t *inc_seg_old, *inc_arr_count, *inc_arr_begin, *inc_arr;
+    int64_t inc_np;     // np the incremental buffers were sized for
     int32_t epoch;      // flag value of the last zeroing launch
 };
 
@@ -103,6 +107,11 @@ void release(mm_sorted *h)
     cudaFree(h->d_status);
     cudaFree(h->d_work);
     cudaFree(h->d_flags);
+    cudaFree(h->perm2);
+    cudaFree(h->inc_seg_old);
+    cudaFree(h->inc_arr_count);
+    cudaFree(h->inc_arr_begin);
+    cudaFree(h->inc_arr);
     if (h->h_status)
         cudaFreeHost(h->h_status);
     delete h;
@@ -340,6 +349,105 @@ mm_status mm_sort_by_cell_async(const mm_grid *g, int order, int k_pad, int64_t 
                                 const double *q, const double *B, void *stream, mm_sorted **inout)
 {
     return sort_common(g, order, k_pad, np, pos, q, B, 0, stream, inout, true);
+}
+
+mm_status mm_resort_by_cell(mm_sorted *h, int64_t np, const double *pos, const double *q, const double *B,
+                            void *stream, int wait)
+{
+    try {
+        if (!h)
+            return fail(MM_ERR_INVALID_ARG, "NULL handle");
+        if (h->pending) {  // the previous sort must be known good: its bins are the starting point
+            mm_status st = mm_sort_wait(h, h->sort_stream);
+            if (st)
+                return st;
+        }
+        if (!h->valid)
+            return fail(MM_ERR_INCOMPATIBLE, "handle holds no valid sort to update");
+        if (np != h->np)
+            return fail(MM_ERR_INCOMPATIBLE, "np (%lld) differs from the handle's sort (%lld)", (long long)np,
+                        (long long)h->np);
+        if ((B != nullptr) != (h->has_B != 0))
+            return fail(MM_ERR_INCOMPATIBLE, "B must be given iff the handle was sorted with B");
+        if (np > 0 && (!pos || !q))
+            return fail(MM_ERR_INVALID_ARG, "pos/q must not be NULL");
+        cudaStream_t s = (cudaStream_t)stream;
+        cudaError_t e = cudaSuccess;
+        if (!h->perm2 || h->inc_np < np) {
+            cudaFree(h->perm2);
+            cudaFree(h->inc_seg_old);
+            cudaFree(h->inc_arr_count);
+            cudaFree(h->inc_arr_begin);
+            cudaFree(h->inc_arr);
+            h->perm2 = h->inc_seg_old = h->inc_arr_count = h->inc_arr_begin = h->inc_arr = nullptr;
+            h->inc_np = 0;
+            const size_t nb = (size_t)(h->nbins > 0 ? h->nbins : 1), n = (size_t)(np > 0 ? np : 1);
+            e = cudaMalloc((void **)&h->perm2, sizeof(int32_t) * (size_t)h->cap_rec);
+            if (!e) e = cudaMalloc((void **)&h->inc_seg_old, sizeof(int32_t) * (nb + 1));
+            if (!e) e = cudaMalloc((void **)&h->inc_arr_count, sizeof(int32_t) * nb);
+            if (!e) e = cudaMalloc((void **)&h->inc_arr_begin, sizeof(int32_t) * (nb + 1));
+            if (!e) e = cudaMalloc((void **)&h->inc_arr, sizeof(int32_t) * n);
+            if (e)
+                return cuda_fail(e, "mm_resort_by_cell allocation");
+            h->inc_np = np;
+        }
+        mm::SortBufs b;
+        b.np = np;
+        b.nbins = h->nbins;
+        b.k_pad = h->k_pad;
+        b.pos = pos;
+        b.q = q;
+        b.B = B;
+        b.f32 = 0;
+        b.key = h->key;
+        b.rank = h->rank;
+        b.count = h->count;
+        b.seg_begin = h->seg_begin;
+        b.perm = h->perm2;  // the new permutation
+        b.rec = h->rec;
+        b.scan_tmp = h->scan_tmp;
+        b.mid_list = h->mid_list;
+        b.huge_list = h->huge_list;
+        b.status = h->d_status;
+        b.capacity = h->cap_rec;
+        mm::IncBufs ib;
+        ib.perm_old = h->perm;
+        ib.seg_old = h->inc_seg_old;
+        ib.arr_count = h->inc_arr_count;
+        ib.arr_begin = h->inc_arr_begin;
+        ib.arr = h->inc_arr;
+        h->valid = 0;
+        e = mm::resort_enqueue(mm::make_geo(h->g, h->order), b, ib, s);
+        if (e)
+            return cuda_fail(e, "mm_resort_by_cell");
+        int32_t *t = h->perm;  // stream order: later work sees the new buffer
+        h->perm = h->perm2;
+        h->perm2 = t;
+        h->valid = 1;
+        if (!wait) {
+            h->pending = 1;
+            h->sort_stream = stream;
+            return MM_OK;
+        }
+        e = cudaMemcpyAsync(h->h_status, h->d_status, sizeof(int32_t) * mm::ST_WORDS, cudaMemcpyDeviceToHost, s);
+        if (!e)
+            e = cudaMemsetAsync(h->d_status + mm::ST_STICKY, 0, sizeof(int32_t), s);
+        if (!e)
+            e = cudaStreamSynchronize(s);
+        if (e)
+            return cuda_fail(e, "mm_resort_by_cell");
+        const int err = h->h_status[mm::ST_ERR];
+        if (err) {
+            h->valid = 0;
+            if (err & mm::ERR_NONFINITE)
+                return fail(MM_ERR_NONFINITE, "NaN/Inf in particle positions, charges or B");
+            return fail(MM_ERR_DOMAIN, "particle outside the owned cell slab");
+        }
+        h->np_padded = h->h_status[mm::ST_NPAD];
+        return MM_OK;
+    } catch (...) {
+        return fail(MM_ERR_CUDA, "unexpected exception in mm_resort_by_cell");
+    }
 }
 
 mm_status mm_sort_wait(mm_sorted *h, void *stream)

@@ -65,6 +65,16 @@ struct SortBufs {
 };
 int64_t scan_tmp_elems(int64_t nbins);
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s);
+// incremental re-binning (mm_resort_by_cell): SortBufs of the handle (perm = the NEW permutation
+// buffer) plus the previous sort's permutation and scratch
+struct IncBufs {
+    int32_t *perm_old;        // [capacity] the previous sort's permutation (leavers get marked)
+    int32_t *seg_old;         // [nbins + 1] scratch: the previous seg_begin
+    int32_t *arr_count;       // [nbins]
+    int32_t *arr_begin;       // [nbins + 1]
+    int32_t *arr;             // [np] arrivals by bin
+};
+cudaError_t resort_enqueue(const Geo &geo, const SortBufs &b, const IncBufs &ib, cudaStream_t s);
 
 // ---- assembly (mm_assemble_fp64.cu) ----------------------------------------
 struct AsmArgs {

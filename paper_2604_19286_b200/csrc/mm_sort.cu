@@ -687,6 +687,97 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP 
     }
 }
 
+// ---- incremental re-binning (NEXT-1; the "sort & communicate" stage of a PIC
+// cycle): the same particles, moved.  Every particle is re-keyed; only the
+// ones whose bin changed touch the bin counters (leave the old bin, join the new one, get an
+// arrival rank); each bin's member list is then its old (stable, ascending) slice minus the
+// leavers plus its arrivals, and the per-bin fix-up restores ascending order - the result is
+// bit-identical to a fresh sort of the new positions.
+// rank[] holds the previous sort's dest (each particle's old slot) on entry: a mover marks its
+// old slot in the old permutation (-3, so the member pass needs no key lookup) and rank[] then
+// carries its arrival rank (-2 for a stayer, -1 for a particle outside the grid) until the
+// fix-up rewrites dest
+template <typename TP>
+__global__ void __launch_bounds__(256) k_rekey(Geo g, int64_t np, const TP *__restrict__ pos,
+                                               uint32_t *__restrict__ key, int32_t *__restrict__ rank,
+                                               int32_t *__restrict__ count, int32_t *__restrict__ arr_count,
+                                               int32_t *__restrict__ perm_old, int32_t *__restrict__ status)
+{
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np)
+        return;
+    int err = 0;
+    uint32_t kn = 0xffffffffu;
+    const double x0 = (double)__ldg(pos + 3 * p), x1 = (double)__ldg(pos + 3 * p + 1),
+                 x2 = (double)__ldg(pos + 3 * p + 2);
+    const uint32_t ko = key[p];
+    Located L = locate(g, x0, x1, x2);
+    if (L.err)
+        err = L.err;
+    else
+        kn = bin_of(g, L);
+    int r = -2;
+    if (kn != ko) {
+        if (ko != 0xffffffffu) {
+            atomicSub(&count[ko], 1);
+            perm_old[rank[p]] = -3;  // leaver
+        }
+        if (kn != 0xffffffffu) {
+            atomicAdd(&count[kn], 1);
+            r = atomicAdd(&arr_count[kn], 1);
+        }
+        key[p] = kn;
+    }
+    rank[p] = kn == 0xffffffffu ? -1 : r;
+    if (err) {
+        atomicOr(&status[ST_ERR], err);
+        atomicOr(&status[ST_STICKY], err);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_arrive(int64_t np, const uint32_t *__restrict__ key,
+                                                const int32_t *__restrict__ rank, const int32_t *__restrict__ arr_begin,
+                                                int32_t *__restrict__ arr)
+{
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np)
+        return;
+    const int r = rank[p];
+    if (r >= 0)
+        arr[arr_begin[key[p]] + r] = (int32_t)p;
+}
+
+// warp per bin: the old slice's stayers (still keyed to this bin) in their old ascending order,
+// then the bin's arrivals; the fix-up sorts the slice
+__global__ void __launch_bounds__(256) k_members(int64_t nbins, const int32_t *__restrict__ seg_old,
+                                                 const int32_t *__restrict__ perm_old,
+                                                 const uint32_t *__restrict__ key,
+                                                 const int32_t *__restrict__ arr_begin,
+                                                 const int32_t *__restrict__ arr_count,
+                                                 const int32_t *__restrict__ arr,
+                                                 const int32_t *__restrict__ seg_begin, int32_t *__restrict__ perm)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t bin = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); bin < nbins; bin += nw) {
+        const int o0 = seg_old[bin], o1 = seg_old[bin + 1];
+        int out = seg_begin[bin];
+        for (int i = o0; i < o1; i += 32) {
+            const int pp = i + lane < o1 ? perm_old[i + lane] : -1;
+            const bool stay = pp >= 0;  // leavers were marked -3 by k_rekey
+            const unsigned b = __ballot_sync(0xffffffffu, stay);
+            if (stay)
+                perm[out + __popc(b & ((1u << lane) - 1u))] = pp;
+            out += __popc(b);
+            if (__ballot_sync(0xffffffffu, pp == -1 && i + lane < o1))
+                break;  // the padding (-1, not a leaver's -3) ends the old members
+        }
+        const int a0 = arr_begin[bin], na = arr_count[bin];
+        for (int j = lane; j < na; j += 32)
+            perm[out + j] = arr[a0 + j];
+    }
+}
+
 inline unsigned blocks_for(int64_t n, int t)
 {
     return (unsigned)((n + t - 1) / t);
@@ -740,38 +831,14 @@ int64_t scan_tmp_elems(int64_t nbins)
     return (nbins + SCAN_TILE - 1) / SCAN_TILE + 1;
 }
 
-cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
+// The per-bin fix-up (ascending original indices = stable order, dest, K padding) and the
+// record scatter, shared by the full and the incremental sort.
+template <typename PT>
+cudaError_t fixup_scatter_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s, PT &pt)
 {
     cudaError_t e;
-    PhaseTimer pt(s);
-    if ((e = cudaMemsetAsync(b.count, 0, sizeof(int32_t) * (size_t)b.nbins, s)))
-        return e;
-    if ((e = cudaMemsetAsync(b.status, 0, sizeof(int32_t) * ST_PER_SORT, s)))
-        return e;
     const int T = 256;
     const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
-
-    if (b.np > 0) {
-        if (b.f32)
-            k_key<float><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(
-                geo, b.np, reinterpret_cast<const float *>(b.pos), b.key, b.rank, b.count, b.status);
-        else
-            k_key<double><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank,
-                                                                              b.count, b.status);
-        count_launch();
-        pt.mark("key");
-    }
-    const int nblk = (int)((b.nbins + SCAN_TILE - 1) / SCAN_TILE);
-    k_scan_local<<<nblk, SCAN_T, 0, s>>>(b.count, b.nbins, b.k_pad, b.seg_begin, b.scan_tmp);
-    k_scan_top<<<1, SCAN_T, 0, s>>>(b.scan_tmp, nblk, b.seg_begin + b.nbins, b.status);
-    k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
-    count_launch(3);
-    pt.mark("scan");
-    if (b.np > 0) {
-        k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
-        count_launch();
-        pt.mark("place");
-    }
     int32_t *dest = b.rank;
     {
         int64_t want = (b.nbins + FIX_WARPS - 1) / FIX_WARPS;
@@ -827,6 +894,80 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
         pt.mark("scatter");
     }
     return cudaGetLastError();
+}
+
+cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
+{
+    cudaError_t e;
+    PhaseTimer pt(s);
+    if ((e = cudaMemsetAsync(b.count, 0, sizeof(int32_t) * (size_t)b.nbins, s)))
+        return e;
+    if ((e = cudaMemsetAsync(b.status, 0, sizeof(int32_t) * ST_PER_SORT, s)))
+        return e;
+    const int T = 256;
+    if (b.np > 0) {
+        if (b.f32)
+            k_key<float><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(
+                geo, b.np, reinterpret_cast<const float *>(b.pos), b.key, b.rank, b.count, b.status);
+        else
+            k_key<double><<<blocks_for((b.np + 32 * KEY_R - 1) / (32 * KEY_R) * 32, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank,
+                                                                              b.count, b.status);
+        count_launch();
+        pt.mark("key");
+    }
+    const int nblk = (int)((b.nbins + SCAN_TILE - 1) / SCAN_TILE);
+    k_scan_local<<<nblk, SCAN_T, 0, s>>>(b.count, b.nbins, b.k_pad, b.seg_begin, b.scan_tmp);
+    k_scan_top<<<1, SCAN_T, 0, s>>>(b.scan_tmp, nblk, b.seg_begin + b.nbins, b.status);
+    k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
+    count_launch(3);
+    pt.mark("scan");
+    if (b.np > 0) {
+        k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
+        count_launch();
+        pt.mark("place");
+    }
+    return fixup_scatter_enqueue(geo, b, s, pt);
+}
+
+cudaError_t resort_enqueue(const Geo &geo, const SortBufs &b, const IncBufs &ib, cudaStream_t s)
+{
+    cudaError_t e;
+    PhaseTimer pt(s);
+    if ((e = cudaMemsetAsync(b.status, 0, sizeof(int32_t) * ST_PER_SORT, s)))
+        return e;
+    if ((e = cudaMemsetAsync(ib.arr_count, 0, sizeof(int32_t) * (size_t)b.nbins, s)))
+        return e;
+    if ((e = cudaMemcpyAsync(ib.seg_old, b.seg_begin, sizeof(int32_t) * (size_t)(b.nbins + 1),
+                             cudaMemcpyDeviceToDevice, s)))
+        return e;
+    const int T = 256;
+    if (b.np > 0) {
+        k_rekey<double><<<blocks_for(b.np, T), T, 0, s>>>(geo, b.np, b.pos, b.key, b.rank, b.count, ib.arr_count,
+                                                           ib.perm_old, b.status);
+        count_launch();
+    }
+    pt.mark("rekey");
+    const int nblk = (int)((b.nbins + SCAN_TILE - 1) / SCAN_TILE);
+    k_scan_local<<<nblk, SCAN_T, 0, s>>>(b.count, b.nbins, b.k_pad, b.seg_begin, b.scan_tmp);
+    k_scan_top<<<1, SCAN_T, 0, s>>>(b.scan_tmp, nblk, b.seg_begin + b.nbins, b.status);
+    k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
+    // arrivals: plain exclusive scan (k_pad 1); its total goes to scratch status words
+    k_scan_local<<<nblk, SCAN_T, 0, s>>>(ib.arr_count, b.nbins, 1, ib.arr_begin, b.scan_tmp);
+    k_scan_top<<<1, SCAN_T, 0, s>>>(b.scan_tmp, nblk, ib.arr_begin + b.nbins, b.status + ST_STICKY + 1);
+    k_scan_add<<<nblk, SCAN_T, 0, s>>>(ib.arr_begin, b.nbins, b.scan_tmp);
+    count_launch(6);
+    pt.mark("scans");
+    if (b.np > 0)
+        k_arrive<<<blocks_for(b.np, T), T, 0, s>>>(b.np, b.key, b.rank, ib.arr_begin, ib.arr);
+    {
+        const int64_t want = (b.nbins + 7) / 8;
+        const unsigned grid = (unsigned)(want < 148 * 16 ? (want < 1 ? 1 : want) : 148 * 16);
+        k_members<<<grid, T, 0, s>>>(b.nbins, ib.seg_old, ib.perm_old, b.key, ib.arr_begin, ib.arr_count, ib.arr,
+                                     b.seg_begin, b.perm);
+    }
+    count_launch(2);
+    pt.mark("members");
+    return fixup_scatter_enqueue(geo, b, s, pt);
 }
 
 }  // namespace mm
