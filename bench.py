@@ -488,6 +488,44 @@ def main():
         sort_nearly_ms = n0.elapsed_time(n1) / 20
         mm.mm_free(hn)
         del hn, dn, ddn
+    # NEXT-1: incremental re-binning (mm_resort_by_cell) of the c2 particles when a random 7% of
+    # them move to a neighbouring cell per step (two position sets alternated), vs the full sort
+    resort = None
+    if world == 1:
+        cfgr, gridr, dr, ddr = setup("c2")
+        gen = torch.Generator(device=dev).manual_seed(5)
+        Lr = torch.tensor(cfgr.n, dtype=torch.float64, device=dev)
+        npr = ddr["q"].shape[0]
+        sel = (torch.rand(npr, device=dev, generator=gen) < 0.10)[:, None]
+        hop = torch.where(torch.rand(npr, 3, device=dev, generator=gen) < 0.5, -1.0, 1.0)
+        hop = hop * (torch.rand(npr, 3, device=dev, generator=gen) < 0.34)
+        moved = torch.remainder(ddr["pos"] + sel * hop, Lr)
+        moved = torch.where(moved >= Lr, torch.zeros_like(moved), moved)
+        nmov = int(((torch.floor(moved) != torch.floor(ddr["pos"])).any(dim=1)).sum().item())
+        hr = mm.mm_sort_by_cell(gridr, 1, 4, ddr["pos"], ddr["q"], ddr["B"])
+        sets = [moved, ddr["pos"]]
+        for k in range(4):
+            mm.mm_resort_by_cell(hr, sets[k % 2], ddr["q"], ddr["B"], wait=False)
+        nrs = max(10, args.steps // 10)
+        barrier()
+        n0.record()
+        for k in range(nrs):
+            mm.mm_resort_by_cell(hr, sets[k % 2], ddr["q"], ddr["B"], wait=False)
+        n1.record()
+        barrier()
+        mm.mm_sort_wait(hr)
+        t_inc = n0.elapsed_time(n1) / nrs
+        n0.record()
+        for k in range(nrs):
+            hr = mm.mm_sort_by_cell(gridr, 1, 4, sets[k % 2], ddr["q"], ddr["B"], handle=hr, wait=False)
+        n1.record()
+        barrier()
+        mm.mm_sort_wait(hr)
+        t_full = n0.elapsed_time(n1) / nrs
+        resort = {"workload": "c2, a random 7% of the particles moved to a neighbouring cell per step",
+                  "moved_particles": nmov, "incremental_ms": t_inc, "full_async_sort_ms": t_full}
+        mm.mm_free(hr)
+        del moved, sets, hop, sel
     r1 = measure("c2", True)
     cfg = r1["cfg"]
     ppc = synth.ppc_of(cfg)
@@ -544,6 +582,7 @@ def main():
                           "step_sort": "mm_sort_by_cell" if args.sync_sort else "mm_sort_by_cell_async + mm_sort_wait",
                           "assemble_ms": r1["assemble_ms"],
                           "sort_nearly_sorted_input_ms": sort_nearly_ms,
+                          "resort": resort,
                           "sort_mps": r1["np"] / (r1["sort_ms"] / 1e3) / 1e6 if r1.get("sort_ms") else None,
                           # sort against the HBM roofline: algorithmic bytes = 24 B (positions, key
                           # pass) + 56 B (pos, q, B, record pass) read + 64 B record written
