@@ -234,7 +234,7 @@ struct PP {
 // tiles as TF32: element (row m, k) at (m >> 3) 1024 + (m & 7) 128 + ((k >> 2) ^ (m & 7)) 16 +
 // (k & 3) 4.  For a fixed row the 32 lanes hit 32 distinct banks (no staging round trip).
 template <int ORDER, int NC, bool X3, int ROLE>
-__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t op_s, int pj,
+__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, unsigned char *op, int pj,
                                           const uint32_t (&lo8)[8], float fws, float fsig)
 {
     using T = PP<ORDER, NC, X3>;
@@ -264,23 +264,23 @@ __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, 
     // tile row m = NB pj + r (X) | MB pj + r - NX (Z): m & 7 is a compile-time constant, so the
     // rows are visited grouped by their swizzle phase and each lane offset lo8[m & 7] is used
     // from one register at a time; m >> 3 splits into a per-slot base plus a constant
-    const uint32_t base_x = op_s + T::A_BYTES + (uint32_t)(T::NB / 8 * pj) * 1024;
-    const uint32_t base_z = op_s + (uint32_t)(T::MB / 8 * pj) * 1024;
+    unsigned char *base_x = op + T::A_BYTES + (T::NB / 8 * pj) * 1024;
+    unsigned char *base_z = op + (T::MB / 8 * pj) * 1024;
 #pragma unroll
     for (int r7 = 0; r7 < 8; ++r7) {
-        const uint32_t lo = lo8[r7];
+        // one register base per (swizzle phase, X | Z block); the row's atom offset is an immediate
+        unsigned char *lx = base_x + lo8[r7], *lz = base_z + lo8[r7];
 #pragma unroll
         for (int r = R0; r < R1; ++r) {
             const int mr = r < T::NX ? r : r - T::NX;  // row inside the bin's X or Z block
             if ((mr & 7) != r7)
                 continue;
             const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-            const uint32_t d = (r < T::NX ? base_x : base_z) + (uint32_t)(mr >> 3) * 1024 + lo;
+            unsigned char *d = (r < T::NX ? lx : lz) + (mr >> 3) * 1024;
             const uint32_t hi = tf32_rna(v);
-            asm volatile("st.shared.b32 [%0], %1;" ::"r"(d), "r"(hi) : "memory");
+            *reinterpret_cast<uint32_t *>(d) = hi;
             if (X3)
-                asm volatile("st.shared.b32 [%0], %1;" ::"r"(d + T::PART_BYTES), "r"(tf32_rna(v - __uint_as_float(hi)))
-                             : "memory");
+                *reinterpret_cast<uint32_t *>(d + T::PART_BYTES) = tf32_rna(v - __uint_as_float(hi));
         }
     }
     }
@@ -377,13 +377,15 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
     for (int r7 = 0; r7 < 8; ++r7)
         lo8[r7] = (uint32_t)((((lane >> 2) ^ r7) << 4) + (lane & 3) * 4 + r7 * 128);
     const bool issuer = role == 0 && lane == 0;
+    static_assert(T::CH == 32, "4 K-steps per chunk");
     uint64_t *bar_buf = bar + 2 * pj, *bar_acc = bar + 2 * T::BPC + pj;
     constexpr uint32_t IDESC_J = idesc_tf32(T::NB);
     uint32_t cc = 0, bc = 0;  // chunks / non-empty bins of this slot
-    const int64_t ngroups = (nbins + T::BPC - 1) / T::BPC;
-    auto range = [&](int64_t grp, int &bb, int &nn) {
-        const int64_t bin = grp * T::BPC + pj;
-        const bool ok = grp < ngroups && bin < nbins;
+    const int nbins32 = (int)nbins;  // < 2^31 (mm_sort_by_cell)
+    const int ngroups = (nbins32 + T::BPC - 1) / T::BPC;
+    auto range = [&](int grp, int &bb, int &nn) {
+        const int bin = grp * T::BPC + pj;
+        const bool ok = grp < ngroups && bin < nbins32;
         bb = ok ? __ldg(seg_begin + bin) : 0;
         nn = ok ? __ldg(seg_begin + bin + 1) - bb : 0;
     };
@@ -398,11 +400,11 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
     };
     int b0, nb, nb0, nnb;
     range(blockIdx.x, b0, nb);
-    range((int64_t)blockIdx.x + gridDim.x, nb0, nnb);
+    range((int)(blockIdx.x + gridDim.x), nb0, nnb);
     double4 ra = make_double4(0, 0, 0, 0), rb = ra;
     load_rec(b0, nb, 0, ra, rb);
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
-        const int64_t bin = grp * T::BPC + pj;
+    for (int grp = blockIdx.x; grp < ngroups; grp += gridDim.x) {
+        const int bin = grp * T::BPC + pj;
         const int nch = (nb + T::CH - 1) / T::CH;
         if (nch == 0)  // nothing was prefetched for the successor yet
             load_rec(nb0, nnb, 0, ra, rb);
@@ -419,12 +421,11 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             // ---- prep + TF32 tiles of this warp's row share (compile-time row range per role)
             {
                 const bool live = T::CH * c + lane < nb;
-                const uint32_t op_s = smem_u32(op);
                 switch (role) {
-                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
-                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
-                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
-                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op_s, pj, lo8, fws, fsig); break;
+                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op, pj, lo8, fws, fsig); break;
+                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op, pj, lo8, fws, fsig); break;
+                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op, pj, lo8, fws, fsig); break;
+                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op, pj, lo8, fws, fsig); break;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -432,16 +433,18 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             if (issuer) {
                 tc_fence_after();
                 const int nks = (min(T::CH, nb - T::CH * c) + 7) / 8;
-                for (int ks = 0; ks < nks; ++ks) {
-                    const unsigned char *Ah = op + ks * 32;                                 // K-step: +32 B
-                    const unsigned char *Bh = op + T::A_BYTES + T::NB * pj * 128 + ks * 32;  // slot's N rows
-                    const int acc0 = (c > 0 || ks > 0) ? 1 : 0;
-                    const uint32_t d = tmem + T::NB * pj;
-                    umma_tf32(d, umma_desc_sw128(Ah), umma_desc_sw128(Bh), IDESC_J, acc0);
-                    if (X3) {
-                        const unsigned char *Al = Ah + T::PART_BYTES, *Bl = Bh + T::PART_BYTES;
-                        umma_tf32(d, umma_desc_sw128(Ah), umma_desc_sw128(Bl), IDESC_J, 1);
-                        umma_tf32(d, umma_desc_sw128(Al), umma_desc_sw128(Bh), IDESC_J, 1);
+                // descriptors: the start-address field (bits 0-13, 16-B units) advances by 2 per
+                // K-step (+32 B inside the swizzled row) and by PART_BYTES / 16 to the low parts
+                const uint64_t dA = umma_desc_sw128(op), dB = umma_desc_sw128(op + T::A_BYTES + T::NB * pj * 128);
+                const uint32_t d = tmem + T::NB * pj;
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    if (ks < nks) {
+                        umma_tf32(d, dA + 2 * ks, dB + 2 * ks, IDESC_J, (c > 0 || ks > 0) ? 1 : 0);
+                        if (X3) {
+                            umma_tf32(d, dA + 2 * ks, dB + 2 * ks + (T::PART_BYTES >> 4), IDESC_J, 1);
+                            umma_tf32(d, dA + 2 * ks + (T::PART_BYTES >> 4), dB + 2 * ks, IDESC_J, 1);
+                        }
                     }
                 }
                 umma_commit(&bar_buf[buf]);
@@ -452,12 +455,12 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
         const int nbk = nb;
         b0 = nb0;
         nb = nnb;
-        range(grp + 2 * (int64_t)gridDim.x, nb0, nnb);
-        if (nch == 0 || bin >= nbins)
+        range(grp + 2 * (int)gridDim.x, nb0, nnb);
+        if (nch == 0 || bin >= nbins32)
             continue;
         // ---- epilogue of this slot's bin: accumulators -> epi[pj][x][z]
         {
-            const int bxl = (int)(bin / plane), rem = (int)(bin - (int64_t)bxl * plane), bx = g.bx0 + bxl;
+            const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
             const int by = rem / g.n2, bz = rem - by * g.n2;
             if (ORDER == 1) {
                 if (role == 0 && lane < 8) {  // node rows a = lane of this bin, read by the deposit
