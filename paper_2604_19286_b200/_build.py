@@ -19,7 +19,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++17", "-O3", "-lineinfo", "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
          "-I", os.path.join(ROOT, "include"), "-ldl"]
-LIB_SOURCES = ["mm_api.cu", "mm_sort.cu", "mm_assemble_fp64.cu", "mm_assemble_o1t.cu", "mm_assemble_tf32.cu", "mm_apply.cu", "mm_halo.cu", "mm_comm.cu", "mm_moments.cu"]
+LIB_SOURCES = ["mm_api.cu", "mm_sort.cu", "mm_assemble_fp64.cu", "mm_assemble_o1t.cu", "mm_assemble_tf32.cu", "mm_apply.cu", "mm_halo.cu", "mm_comm.cu", "mm_moments.cu", "mm_nodesum.cu"]
 PROBE_SOURCES = ["mm_probe.cu"]
 _lock = threading.Lock()
 

@@ -43,6 +43,11 @@ struct mm_sorted {
     int32_t *inc_seg_old, *inc_arr_count, *inc_arr_begin, *inc_arr;
     int64_t inc_np;     // np the incremental buffers were sized for
     int32_t epoch;      // flag value of the last zeroing launch
+    double *rec_tmp;    // record-first sort scratch [cap_rec][8] (inputs beyond L2, lazily allocated)
+    int64_t cap_tmp;
+    int dest_valid;     // rank[] holds the inverse permutation (classic path); else the atomic ranks
+    void *d_dblk;       // two-phase deposit: per-bin pair-product blocks (lazily allocated)
+    size_t dblk_bytes;
 };
 
 namespace {
@@ -107,6 +112,8 @@ void release(mm_sorted *h)
     cudaFree(h->d_status);
     cudaFree(h->d_work);
     cudaFree(h->d_flags);
+    cudaFree(h->d_dblk);
+    cudaFree(h->rec_tmp);
     cudaFree(h->perm2);
     cudaFree(h->inc_seg_old);
     cudaFree(h->inc_arr_count);
@@ -287,6 +294,26 @@ mm_status sort_common(const mm_grid *g, int order, int k_pad, int64_t np, const 
         b.huge_list = h->huge_list;
         b.status = h->d_status;
         b.capacity = h->cap_rec;
+        // record-first path from MM_SORT_RECFIRST_MIN particles on (default 48 M: beyond L2 the
+        // classic path's random 4-B passes dominate)
+        const char *rfm = getenv("MM_SORT_RECFIRST_MIN");  // read per call (tests, A/B)
+        const int64_t recfirst_min = rfm ? (int64_t)atoll(rfm) : (int64_t)48 * 1000 * 1000;
+        if (np >= recfirst_min && np > 0) {
+            if (h->cap_tmp < h->cap_rec) {
+                cudaFree(h->rec_tmp);
+                h->rec_tmp = nullptr;
+                h->cap_tmp = 0;
+                e = cudaMalloc((void **)&h->rec_tmp, sizeof(double) * 8 * (size_t)h->cap_rec);
+                if (e) {
+                    if (fresh)
+                        release(h);
+                    return cuda_fail(e, "mm_sort_by_cell allocation");
+                }
+                h->cap_tmp = h->cap_rec;
+            }
+            b.rec_tmp = h->rec_tmp;
+        }
+        h->dest_valid = b.rec_tmp ? 0 : 1;
         e = mm::sort_enqueue(mm::make_geo(*g, order), b, s);
         if (async) {
             // no host round trip: the status stays on the device (sticky error word) until
@@ -417,6 +444,12 @@ mm_status mm_resort_by_cell(mm_sorted *h, int64_t np, const double *pos, const d
         ib.arr_begin = h->inc_arr_begin;
         ib.arr = h->inc_arr;
         h->valid = 0;
+        if (!h->dest_valid) {  // the record-first sort left the atomic ranks in rank[]
+            e = mm::inverse_enqueue(h->perm, h->seg_begin + h->nbins, h->cap_rec, h->rank, s);
+            if (e)
+                return cuda_fail(e, "mm_resort_by_cell");
+            h->dest_valid = 1;
+        }
         e = mm::resort_enqueue(mm::make_geo(h->g, h->order), b, ib, s);
         if (e)
             return cuda_fail(e, "mm_resort_by_cell");
@@ -534,7 +567,7 @@ mm_status check_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, co
 // work counter (zeroed by the caller).
 cudaError_t enqueue_range(const mm_sorted *h, mm::Geo geo, mm_kind kind, mm_precision prec, const mm_species *sp,
                           void *out, void *ghost, int bx_lo, int bx_hi, int work_idx, cudaStream_t s,
-                          int32_t *zflags = nullptr, int32_t zepoch = 0)
+                          int32_t *zflags = nullptr, int32_t zepoch = 0, void *dblk = nullptr)
 {
     const int64_t plane = (int64_t)h->g.n[1] * h->g.n[2];
     if (bx_hi <= bx_lo)
@@ -553,9 +586,26 @@ cudaError_t enqueue_range(const mm_sorted *h, mm::Geo geo, mm_kind kind, mm_prec
     a.ghost = geo.periodic_x ? nullptr : static_cast<double *>(ghost);
     a.zflags = zflags;
     a.zepoch = zepoch;
+    a.dblk = dblk ? static_cast<char *>(dblk) + (prec == MM_FP64 ? 8 : 4) * plane * bx_lo *
+                                                     mm::block_elems(h->order, (int)kind)
+                  : nullptr;
     if (prec == MM_FP64)
         return mm::assemble_fp64_enqueue(geo, a, s);
     return mm::assemble_tf32_enqueue(geo, a, prec == MM_TF32X3 ? 1 : 0, s);
+}
+
+// Two-phase deposit (mm_nodesum.cu) over the whole bin range: the assembly kernel stores one
+// pair-product block per bin, a node-row kernel sums them (no REDs, no zero-fill).  Measured
+// slower than the RED deposit on every config (the node kernel is L1-bound), so
+// it is off unless MM_TWO_PHASE (read per call) selects it: bit 0 TF32 order 2, bit 1 TF32
+// order 1, bit 2 FP64 order 2, bit 3 (diagnostics) phase 1 alone.  tests/test_gpu_twophase.py.
+bool two_phase(const mm_sorted *h, mm_precision prec)
+{
+    const char *v = getenv("MM_TWO_PHASE");
+    const int mode = v ? atoi(v) : 0;
+    if (prec == MM_FP64)
+        return h->order == 2 && (mode & 4);
+    return h->order == 2 ? (mode & 1) : (mode & 2);
 }
 
 int64_t row_elems(const mm_sorted *h, mm_kind kind)
@@ -616,6 +666,29 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
                 hm->epoch = 1;
             }
             zflags = hm->d_flags;
+        }
+        if (two_phase(h, prec)) {
+            mm_sorted *hm = const_cast<mm_sorted *>(h);
+            const size_t need = esz * (size_t)h->nbins * (size_t)mm::block_elems(h->order, (int)kind);
+            if (hm->dblk_bytes < need) {
+                cudaFree(hm->d_dblk);
+                hm->d_dblk = nullptr;
+                hm->dblk_bytes = 0;
+                e = cudaMalloc(&hm->d_dblk, need);
+                if (e)
+                    return cuda_fail(e, "mm_assemble block buffer");
+                hm->dblk_bytes = need;
+            }
+            e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
+            if (!e)
+                e = enqueue_range(h, geo, kind, prec, sp, out, ghost, 0, geo.nbx, 0, s, nullptr, 0, hm->d_dblk);
+            const char *v = getenv("MM_TWO_PHASE");  // bit 3: phase 1 alone (timing diagnostics)
+            if (!e && !(v && (atoi(v) & 8)))
+                e = mm::nodesum_enqueue(geo, (int)kind, (int)esz, hm->d_dblk, out,
+                                        geo.periodic_x ? nullptr : ghost, accumulate, s);
+            if (e)
+                return cuda_fail(e, "mm_assemble launch");
+            return MM_OK;
         }
         if (!accumulate && !zflags) {
             e = cudaMemsetAsync(out, 0, esz * (size_t)nout, s);

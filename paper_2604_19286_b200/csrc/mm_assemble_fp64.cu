@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
                                                                 const int32_t *__restrict__ seg_begin,
                                                                 int64_t nbins, double wscale, double sigma,
                                                                 double *__restrict__ out, double *__restrict__ ghost,
-                                                                int *__restrict__ work)
+                                                                int *__restrict__ work, double *__restrict__ dblk)
 {
     using L = O2T;
     extern __shared__ __align__(16) double dsm_o2t[];
@@ -259,6 +259,11 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
             }
         }
         if (b0 == b1) {  // empty bin (rare): advance the ticket queue
+            if (dblk) {  // two-phase: an empty bin's block is zero
+                double *dp = dblk + (int64_t)bin * (36 * 54);
+                for (int e = threadIdx.x; e < 36 * 54; e += L::WARPS * 32)
+                    dp[e] = 0.0;
+            }
             __syncthreads();
             if (threadIdx.x == 0) {
                 q[0] = q[1];
@@ -287,7 +292,8 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
         }
         const int bxl = (int)(bin / plane), rem = bin - bxl * plane, bx = g.bx0 + bxl;
         const int by = rem / g.n2, bz = rem - by * g.n2;
-        if (threadIdx.x < 27) {
+        const int fin = bin;
+        if (threadIdx.x < 27 && !dblk) {
             const int a = threadIdx.x;
             rowp[a] = row_ptr(g, g.x_begin + bx - 1 + a / 9, wrapi(by + (a / 3) % 3, g.n1), wrapi(bz + a % 3, g.n2),
                               out, ghost, RL);
@@ -300,6 +306,13 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
         }
         __syncthreads();
         bin = q[0];
+        if (dblk) {
+            // two-phase deposit (mm_nodesum.cu): the stage is the bin's block D[X row][Z col]
+            double *dp = dblk + (int64_t)fin * (36 * 54);
+            for (int e = threadIdx.x; e < 36 * 54; e += L::WARPS * 32)
+                dp[e] = stage[e];
+            continue;
+        }
         // ---- flush: runs of 27 contiguous doubles (b_z x comps) of node a's row, three runs
         //      (b_y = 0..2, 5 slots apart) per unit (a, b_x).  The next writes of stage / rowp /
         //      q come after the next chunk barrier.
@@ -350,7 +363,8 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                                                                    const int32_t *__restrict__ seg_begin,
                                                                    int64_t nbins, int rs, double sigma,
                                                                    double *__restrict__ out,
-                                                                   double *__restrict__ ghost)
+                                                                   double *__restrict__ ghost,
+                                                                   double *__restrict__ dblk)
 {
     using L = PPS<ORDER>;
     extern __shared__ __align__(16) double dsm_pps[];
@@ -496,6 +510,15 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                     if (x < L::NX && z < L::NZ)
                         stage[x * L::NZ + z] = acc[mt][v];
                 }
+            if (dblk) {
+                // two-phase deposit (mm_nodesum.cu): the stage is the bin's block D[x][z]
+                __syncwarp();
+                double *dp = dblk + (int64_t)bin * (L::NX * L::NZ);
+                for (int e = lane; e < L::NX * L::NZ; e += 32)
+                    dp[e] = stage[e];
+                __syncwarp();
+                goto next_bin;
+            }
             const int bx = g.bx0 + cx, by = cy, bz = cz;
             if (lane < L::NA) {
                 const int a = lane;
@@ -513,9 +536,16 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                     red_add(s_rowp[a] + ((t >> 5) & 127), stage[t >> 12]);
             }
             // (the stage spans X rows only, which every chunk's prep rewrites)
-        } else if (bin + nw < nbins && nb0 + lane < nb1) {
-            ra = ld256(rec + rs * (int64_t)(nb0 + lane));
+        } else {
+            if (dblk) {  // two-phase: an empty bin's block is zero
+                double *dp = dblk + (int64_t)bin * (L::NX * L::NZ);
+                for (int e = lane; e < L::NX * L::NZ; e += 32)
+                    dp[e] = 0.0;
+            }
+            if (bin + nw < nbins && nb0 + lane < nb1)
+                ra = ld256(rec + rs * (int64_t)(nb0 + lane));
         }
+    next_bin:
         bin += nw;
         cz += wz;
         if (cz >= g.n2) {
@@ -552,7 +582,7 @@ cudaError_t launch_pps(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
     k_asm_pps<ORDER><<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.rec_stride, a.sigma,
-                                                          a.out, a.ghost);
+                                                          a.out, a.ghost, static_cast<double *>(a.dblk));
     count_launch();
     return cudaGetLastError();
 }
@@ -585,7 +615,7 @@ cudaError_t launch_o2t(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(a.nbins < cap ? (a.nbins < 1 ? 1 : a.nbins) : cap);
     k_asm_o2t<<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.wscale, a.sigma, a.out,
-                                                   a.ghost, a.work);
+                                                   a.ghost, a.work, static_cast<double *>(a.dblk));
     count_launch();
     return cudaGetLastError();
 }

@@ -290,7 +290,7 @@ template <int ORDER, int NC, bool X3>
 __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, const double *__restrict__ rec,
                                                   const int32_t *__restrict__ seg_begin, int64_t nbins, int rs,
                                                   double wscale, double sigma, float *__restrict__ out,
-                                                  float *__restrict__ ghost)
+                                                  float *__restrict__ ghost, float *__restrict__ dblk)
 {
     using T = PP<ORDER, NC, X3>;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -456,8 +456,41 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
         b0 = nb0;
         nb = nnb;
         range(grp + 2 * (int)gridDim.x, nb0, nnb);
+        if (dblk && nch == 0 && bin < nbins32) {  // two-phase: an empty bin's block is zero
+            float *dp = dblk + (int64_t)bin * (T::NX * T::NZ);
+            for (int e = 32 * role + lane; e < T::NX * T::NZ; e += 32 * T::WPB)
+                dp[e] = 0.0f;
+        }
         if (nch == 0 || bin >= nbins32)
             continue;
+        if (dblk) {
+            // two-phase deposit (mm_nodesum.cu): the bin's block D[x][z] straight from TMEM to its
+            // slot of the block buffer with coalesced stores (lane = z); no REDs, no staging.  The
+            // next bin's first MMA overwrites these columns only after the slot's next chunk
+            // barrier, which every reader reaches after its tcgen05.wait::ld.
+            mbar_wait(bar_acc, bc & 1);
+            ++bc;
+            tc_fence_after();
+            if (warp < 4) {
+                const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
+                float *dp = dblk + (int64_t)bin * (T::NX * T::NZ);
+                const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
+#pragma unroll
+                for (int x0 = 0; x0 < T::NX; x0 += 16) {
+                    float v[16];
+                    tmem_ld16(tl + x0, v);
+                    tmem_wait_ld();
+                    if (z < T::NZ) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (x0 + i < T::NX)
+                                dp[(x0 + i) * T::NZ + z] = v[i];
+                    }
+                }
+            }
+            tc_fence_before();
+            continue;
+        }
         // ---- epilogue of this slot's bin: accumulators -> epi[pj][x][z]
         {
             const int bxl = bin / plane, rem = bin - bxl * plane, bx = g.bx0 + bxl;
@@ -567,7 +600,7 @@ cudaError_t launch_tf32(const Geo &geo, const AsmArgs &a, cudaStream_t s)
         grid = ngroups;
     k_asm_tf32<ORDER, NC, X3><<<(unsigned)grid, T::THREADS, T::SMEM, s>>>(
         geo, a.rec, a.seg_begin, a.nbins, a.rec_stride, a.wscale, a.sigma, reinterpret_cast<float *>(a.out),
-        reinterpret_cast<float *>(a.ghost));
+        reinterpret_cast<float *>(a.ghost), reinterpret_cast<float *>(a.dblk));
     count_launch();
     return cudaGetLastError();
 }

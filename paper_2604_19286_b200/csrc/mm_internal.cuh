@@ -62,9 +62,14 @@ struct SortBufs {
     int32_t *huge_list;  // [nbins]
     int32_t *status;     // [ST_WORDS]
     int64_t capacity;
+    double *rec_tmp = nullptr;  // [capacity][8] scratch: the record-first path (inputs beyond L2),
+                                // which leaves rank as the atomic rank (no inverse permutation)
 };
 int64_t scan_tmp_elems(int64_t nbins);
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s);
+// dest[perm[i]] = i for the padded slots i < *seg_end (perm -1 = pad)
+cudaError_t inverse_enqueue(const int32_t *perm, const int32_t *seg_end, int64_t capacity, int32_t *dest,
+                            cudaStream_t s);
 // incremental re-binning (mm_resort_by_cell): SortBufs of the handle (perm = the NEW permutation
 // buffer) plus the previous sort's permutation and scratch
 struct IncBufs {
@@ -90,6 +95,8 @@ struct AsmArgs {
     int *work;            // device work counter, zeroed before the launch
     int32_t *zflags;      // first-writer zeroing (dev::ZeroPlan): row flags, nullptr = output pre-zeroed
     int32_t zepoch;       //   flag value of this launch
+    void *dblk = nullptr; // two-phase deposit: per-bin pair-product blocks [nbins][block_elems]
+                          //   (the kernel stores them; nodesum_enqueue writes the output), else REDs
 };
 cudaError_t assemble_fp64_enqueue(const Geo &geo, const AsmArgs &a, cudaStream_t s);
 // true when the kernel for (order, ncomp, tf32) zeroes its output rows itself (AsmArgs::zflags)
@@ -97,6 +104,14 @@ bool zeroes_inside(int order, int ncomp, int tf32);
 
 // ---- TF32 / 3xTF32 on tcgen05 (mm_assemble_tf32.cu); out/ghost hold FP32 ----------
 cudaError_t assemble_tf32_enqueue(const Geo &geo, const AsmArgs &a, int x3, cudaStream_t s);
+
+// ---- two-phase deposit, phase 2 (mm_nodesum.cu) -------------------------------
+// elements of one bin's pair-product block: (NU^2) x (NU C), NU = 3 | 6
+int64_t block_elems(int order, int ncomp);
+// every owned (and, on a slab, ghost) node row = (accumulate ? row : 0) + the sum of the blocks of
+// the bins around it; D holds elem_bytes-wide blocks of every bin (zero for an empty bin)
+cudaError_t nodesum_enqueue(const Geo &g, int ncomp, int elem_bytes, const void *D, void *out, void *ghost,
+                            int accumulate, cudaStream_t s);
 
 // ---- operator apply (mm_apply.cu) -------------------------------------------
 cudaError_t apply_enqueue(const Geo &geo, int ncomp, const double *M, const double *E, double *y, int accumulate,

@@ -687,6 +687,355 @@ __global__ void __launch_bounds__(256, 3) k_scatter(Geo g, int64_t np, const TP 
     }
 }
 
+// ---- record-first path for inputs beyond L2 ----------------------------------------------
+// Beyond the 126 MB L2 the classic path's two random 4-B passes (k_place: perm[seg + rank] = p;
+// the fix-up's inverse permutation dest[perm[i]] = i) cost 9 of the 14 ms of a 134.7 M-particle
+// sort: random stores are bound by the L2 request rate (one request per lane) whatever their
+// width.  Here the only random pass is the record one:
+//   k_scatter0  coalesced over particles: the 64-B record {xi, q, B, p} goes to its UNSTABLE
+//               slot seg_begin[key] + rank of a scratch buffer (the particle index p in the pad
+//               double), one cp.async.bulk each;
+//   k_fixrec_*  per bin, coalesced: sort the (p, slot) pairs of the bin by p (= stable order),
+//               write perm and the final records (pad double 0; 32-B records without B) in
+//               order, zero the K-padding.
+// The result is bit-identical to the classic path (tests/test_gpu_parity_sort_tf32.py runs
+// both).  The inverse permutation is not produced; mm_resort_by_cell rebuilds it (k_inverse).
+
+template <bool VEC, typename TP>
+__global__ void __launch_bounds__(256, 3) k_scatter0(Geo g, int64_t np, const TP *__restrict__ pos,
+                                                     const double *__restrict__ q, const TP *__restrict__ B,
+                                                     const uint32_t *__restrict__ key,
+                                                     const int32_t *__restrict__ rank,
+                                                     const int32_t *__restrict__ seg_begin,
+                                                     double *__restrict__ tmp, int32_t *__restrict__ status)
+{
+    extern __shared__ __align__(128) double sm_rec0[];  // [256 threads][4 records][8]
+    const int64_t p0 = 4 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x);
+    if (p0 >= np)
+        return;
+    const bool full = p0 + 4 <= np;
+    uint32_t k[4];
+    int r[4];
+    if (full) {
+        const uint4 kk = *reinterpret_cast<const uint4 *>(key + p0);
+        const int4 rr = *reinterpret_cast<const int4 *>(rank + p0);
+        k[0] = kk.x; k[1] = kk.y; k[2] = kk.z; k[3] = kk.w;
+        r[0] = rr.x; r[1] = rr.y; r[2] = rr.z; r[3] = rr.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            k[j] = p0 + j < np ? key[p0 + j] : 0xffffffffu;
+            r[j] = p0 + j < np ? rank[p0 + j] : 0;
+        }
+    }
+    int d[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+        d[j] = k[j] != 0xffffffffu ? __ldg(seg_begin + k[j]) + r[j] : -1;
+    double qq[4], x[12], bb[12];
+    load_vec3x4<VEC>(pos, p0, np, x);
+    if (VEC && full) {
+        const double4 t = ld256(q + p0);
+        qq[0] = t.x; qq[1] = t.y; qq[2] = t.z; qq[3] = t.w;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            qq[j] = p0 + j < np ? q[p0 + j] : 0.0;
+    }
+    if (B) {
+        load_vec3x4<VEC>(B, p0, np, bb);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 12; ++j)
+            bb[j] = 0.0;
+    }
+    int err = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        if (d[j] < 0)
+            continue;
+        Located L = locate(g, x[3 * j], x[3 * j + 1], x[3 * j + 2]);
+        if (!(isfinite(qq[j]) && isfinite(bb[3 * j]) && isfinite(bb[3 * j + 1]) && isfinite(bb[3 * j + 2])))
+            err |= ERR_NONFINITE;
+        double *sr = sm_rec0 + 32 * threadIdx.x + 8 * j;
+        sr[0] = L.xi[0];
+        sr[1] = L.xi[1];
+        sr[2] = L.xi[2];
+        sr[3] = qq[j];
+        sr[4] = bb[3 * j];
+        sr[5] = bb[3 * j + 1];
+        sr[6] = bb[3 * j + 2];
+        sr[7] = __longlong_as_double(p0 + j);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 64;" ::"l"(tmp + 8 * (int64_t)d[j]),
+                     "r"((uint32_t)__cvta_generic_to_shared(sr))
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    if (err) {
+        atomicOr(&status[ST_ERR], err);
+        atomicOr(&status[ST_STICKY], err);
+    }
+}
+
+// Register bitonic network over K = 32 R 64-bit keys (element i = lane + 32 r in v[r]), as
+// bitonic_regs; keys are (particle index << 32 | scratch slot), distinct.
+template <int R>
+__device__ __forceinline__ void bitonic_regs64(uint64_t (&v)[R], int lane)
+{
+    constexpr int K = 32 * R;
+#pragma unroll
+    for (int k = 2; k <= K; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j >= 32) {
+                const int jr = j >> 5;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    if (r & jr)
+                        continue;
+                    const int r2 = r | jr;
+                    const bool up = ((lane + 32 * r) & k) == 0;
+                    const uint64_t lo = min(v[r], v[r2]), hi = max(v[r], v[r2]);
+                    v[r] = up ? lo : hi;
+                    v[r2] = up ? hi : lo;
+                }
+            } else {
+                const bool lower = (lane & j) == 0;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const uint64_t pv = __shfl_xor_sync(0xffffffffu, v[r], j);
+                    const bool up = ((lane + 32 * r) & k) == 0;
+                    v[r] = (lower == up) ? min(v[r], pv) : max(v[r], pv);
+                }
+            }
+        }
+    }
+}
+
+// slot j of the bin (sorted position) <- scratch record src: perm and the final record
+__device__ __forceinline__ void put_rec(const double *__restrict__ tmp, double *__restrict__ rec,
+                                        int32_t *__restrict__ perm, int rs, int64_t j, int64_t src, int32_t p)
+{
+    perm[j] = p;
+    const double4 a = ld256(tmp + 8 * src);
+    st256(rec + rs * j, a.x, a.y, a.z, a.w);
+    if (rs == 8) {
+        const double4 c = ld256(tmp + 8 * src + 4);
+        st256(rec + rs * j + 4, c.x, c.y, c.z, 0.0);
+    }
+}
+
+template <int R>
+__device__ __forceinline__ void fixrec_regs(const double *__restrict__ tmp, double *__restrict__ rec,
+                                            int32_t *__restrict__ perm, int rs, int64_t b, int n, int lane)
+{
+    uint64_t v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        v[r] = i < n ? ((uint64_t)(uint32_t)__double_as_longlong(tmp[8 * (b + i) + 7]) << 32) | (uint32_t)i
+                     : ~0ull;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const uint64_t nx = __shfl_down_sync(0xffffffffu, v[r], 1);
+        const uint64_t first = __shfl_sync(0xffffffffu, v[r + 1 < R ? r + 1 : r], 0);
+        ok = ok && (lane < 31 ? v[r] <= nx : (r + 1 < R ? v[r] <= first : true));
+    }
+    if (!__all_sync(0xffffffffu, ok))
+        bitonic_regs64<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        if (i < n)
+            put_rec(tmp, rec, perm, rs, b + i, b + (uint32_t)v[r], (int32_t)(v[r] >> 32));
+    }
+}
+
+// Bins of 64 < n <= 32 R: the 32-bit network on the particle indices alone (half the work of the
+// 64-bit one), then each element finds its sorted position by binary search in the sorted list
+// (indices are distinct) and leaves its scratch slot there, so the record copies run in order.
+template <int R>
+__device__ __forceinline__ void fixrec_regs32(const double *__restrict__ tmp, double *__restrict__ rec,
+                                              int32_t *__restrict__ perm, int rs, int64_t b, int n, int lane,
+                                              int32_t *__restrict__ sp, int16_t *__restrict__ src)
+{
+    int32_t v[R], o[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        v[r] = o[r] = i < n ? (int32_t)__double_as_longlong(tmp[8 * (b + i) + 7]) : INT_MAX;
+    }
+    bool ok = true;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int32_t nx = __shfl_down_sync(0xffffffffu, v[r], 1);
+        const int32_t first = __shfl_sync(0xffffffffu, v[r + 1 < R ? r + 1 : r], 0);
+        ok = ok && (lane < 31 ? v[r] <= nx : (r + 1 < R ? v[r] <= first : true));
+    }
+    if (__all_sync(0xffffffffu, ok)) {  // already ascending: slot i stays at i
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int i = lane + 32 * r;
+            if (i < n)
+                put_rec(tmp, rec, perm, rs, b + i, b + i, v[r]);
+        }
+        return;
+    }
+    bitonic_regs<R>(v, lane);
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        sp[lane + 32 * r] = v[r];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        if (i < n) {
+            int lo = 0, hi = n;  // first position with sp[pos] >= o[r]
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (sp[mid] < o[r])
+                    lo = mid + 1;
+                else
+                    hi = mid;
+            }
+            src[lo] = (int16_t)i;
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int j = lane + 32 * r;
+        if (j < n)
+            put_rec(tmp, rec, perm, rs, b + j, b + src[j], v[r]);
+    }
+    __syncwarp();  // sp / src are reused by the warp's next bin
+}
+
+constexpr int FIXREC_WARP_MAX = 512;
+
+__global__ void __launch_bounds__(FIX_WARPS * 32) k_fixrec_warp(int64_t nbins, const int32_t *__restrict__ count,
+                                                                const int32_t *__restrict__ seg_begin,
+                                                                const double *__restrict__ tmp,
+                                                                int32_t *__restrict__ perm, double *__restrict__ rec,
+                                                                int32_t *__restrict__ mid_list,
+                                                                int32_t *__restrict__ huge_list,
+                                                                int32_t *__restrict__ status, int rs)
+{
+    __shared__ int32_t s_sp[FIX_WARPS][FIXREC_WARP_MAX];
+    __shared__ int16_t s_src[FIX_WARPS][FIXREC_WARP_MAX];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t nwarps = (int64_t)gridDim.x * FIX_WARPS;
+    for (int64_t bin = (int64_t)blockIdx.x * FIX_WARPS + w; bin < nbins; bin += nwarps) {
+        const int n = count[bin];
+        const int64_t b = seg_begin[bin], e = seg_begin[bin + 1];
+        zero_pads(perm, rec, rs, b + n, e, lane, 32);
+        if (n == 0)
+            continue;
+        if (n > FIXREC_WARP_MAX) {
+            if (lane == 0) {
+                if (n > CTA_BIN_MAX)
+                    huge_list[atomicAdd(&status[ST_NHUGE], 1)] = (int32_t)bin;
+                else
+                    mid_list[atomicAdd(&status[ST_NMID], 1)] = (int32_t)bin;
+            }
+            continue;
+        }
+        if (n <= 64)
+            fixrec_regs<2>(tmp, rec, perm, rs, b, n, lane);
+        else if (n <= 128)
+            fixrec_regs32<4>(tmp, rec, perm, rs, b, n, lane, s_sp[w], s_src[w]);
+        else if (n <= 256)
+            fixrec_regs32<8>(tmp, rec, perm, rs, b, n, lane, s_sp[w], s_src[w]);
+        else
+            fixrec_regs32<16>(tmp, rec, perm, rs, b, n, lane, s_sp[w], s_src[w]);
+    }
+}
+
+// bins of FIXREC_WARP_MAX < n <= CTA_BIN_MAX: bitonic sort of the 64-bit keys in shared memory
+__global__ void __launch_bounds__(1024) k_fixrec_cta(const int32_t *__restrict__ count,
+                                                     const int32_t *__restrict__ seg_begin,
+                                                     const double *__restrict__ tmp, int32_t *__restrict__ perm,
+                                                     double *__restrict__ rec, const int32_t *__restrict__ mid_list,
+                                                     const int32_t *__restrict__ status, int rs)
+{
+    extern __shared__ uint64_t s64[];
+    const int nmid = status[ST_NMID];
+    for (int it = blockIdx.x; it < nmid; it += gridDim.x) {
+        const int32_t bin = mid_list[it];
+        const int n = count[bin];
+        const int64_t b = seg_begin[bin];
+        int N = 1024;
+        while (N < n)
+            N <<= 1;
+        for (int i = threadIdx.x; i < N; i += blockDim.x)
+            s64[i] = i < n ? ((uint64_t)(uint32_t)__double_as_longlong(tmp[8 * (b + i) + 7]) << 32) | (uint32_t)i
+                           : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= N; k <<= 1) {
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < N; i += blockDim.x) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const uint64_t x = s64[i], y = s64[ixj];
+                        const bool up = (i & k) == 0;
+                        if ((x > y) == up) {
+                            s64[i] = y;
+                            s64[ixj] = x;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (int i = threadIdx.x; i < n; i += blockDim.x)
+            put_rec(tmp, rec, perm, rs, b + i, b + (uint32_t)s64[i], (int32_t)(s64[i] >> 32));
+        __syncthreads();
+    }
+}
+
+// bins of more than CTA_BIN_MAX particles (degenerate inputs): stable compaction over the
+// particles; the scratch slot of particle p is seg_begin[key] + rank[p]
+__global__ void __launch_bounds__(1024) k_fixrec_huge(int64_t np, const uint32_t *__restrict__ key,
+                                                      const int32_t *__restrict__ rank,
+                                                      const int32_t *__restrict__ seg_begin,
+                                                      const double *__restrict__ tmp, int32_t *__restrict__ perm,
+                                                      double *__restrict__ rec, const int32_t *__restrict__ huge_list,
+                                                      const int32_t *__restrict__ status, int rs)
+{
+    const int nhuge = status[ST_NHUGE];
+    for (int it = blockIdx.x; it < nhuge; it += gridDim.x) {
+        const uint32_t bin = (uint32_t)huge_list[it];
+        const int64_t b = seg_begin[bin];
+        int64_t out = b;
+        for (int64_t c0 = 0; c0 < np; c0 += blockDim.x) {
+            const int64_t p = c0 + threadIdx.x;
+            const int f = (p < np && key[p] == bin) ? 1 : 0;
+            int total;
+            const int pre = block_excl_scan(f, total);
+            if (f)
+                put_rec(tmp, rec, perm, rs, out + pre, b + rank[p], (int32_t)p);
+            out += total;
+        }
+    }
+}
+
+// dest[perm[i]] = i over the padded slots (mm_resort_by_cell needs the previous sort's inverse
+// permutation; the record-first path does not produce it)
+__global__ void k_inverse(const int32_t *__restrict__ perm, const int32_t *__restrict__ total,
+                          int32_t *__restrict__ dest)
+{
+    const int64_t n = *total;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = perm[i];
+        if (p >= 0)
+            dest[p] = (int32_t)i;
+    }
+}
+
 // ---- incremental re-binning (NEXT-1; the "sort & communicate" stage of a PIC
 // cycle): the same particles, moved.  Every particle is re-keyed; only the
 // ones whose bin changed touch the bin counters (leave the old bin, join the new one, get an
@@ -896,6 +1245,58 @@ cudaError_t fixup_scatter_enqueue(const Geo &geo, const SortBufs &b, cudaStream_
     return cudaGetLastError();
 }
 
+template <typename PT>
+cudaError_t recfirst_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s, PT &pt)
+{
+    cudaError_t e;
+    const int T = 256;
+    const int rs = b.B ? 8 : 4;
+    {
+        constexpr int SMEM0 = 256 * 4 * 64;
+        const unsigned gs = blocks_for((b.np + 3) / 4, T);
+        auto k_d_v = k_scatter0<true, double>, k_d_n = k_scatter0<false, double>;
+        auto k_f_v = k_scatter0<true, float>, k_f_n = k_scatter0<false, float>;
+        if ((e = cudaFuncSetAttribute(k_d_v, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM0)) ||
+            (e = cudaFuncSetAttribute(k_d_n, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM0)) ||
+            (e = cudaFuncSetAttribute(k_f_v, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM0)) ||
+            (e = cudaFuncSetAttribute(k_f_n, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM0)))
+            return e;
+        if (b.f32) {
+            const float *pf = reinterpret_cast<const float *>(b.pos), *bf = reinterpret_cast<const float *>(b.B);
+            const bool v16 = ((uintptr_t)pf % 16 == 0) && ((uintptr_t)bf % 16 == 0) && ((uintptr_t)b.q % 32 == 0);
+            (v16 ? k_f_v : k_f_n)<<<gs, T, SMEM0, s>>>(geo, b.np, pf, b.q, bf, b.key, b.rank, b.seg_begin, b.rec_tmp,
+                                                       b.status);
+        } else {
+            const bool vec = ((uintptr_t)b.pos % 32 == 0) && ((uintptr_t)b.q % 32 == 0) && ((uintptr_t)b.B % 32 == 0);
+            (vec ? k_d_v : k_d_n)<<<gs, T, SMEM0, s>>>(geo, b.np, b.pos, b.q, b.B, b.key, b.rank, b.seg_begin,
+                                                       b.rec_tmp, b.status);
+        }
+        count_launch();
+        pt.mark("scatter0");
+    }
+    {
+        const int64_t want = (b.nbins + FIX_WARPS - 1) / FIX_WARPS;
+        const unsigned grid = (unsigned)(want < 148 * 16 ? (want < 1 ? 1 : want) : 148 * 16);
+        k_fixrec_warp<<<grid, FIX_WARPS * 32, 0, s>>>(b.nbins, b.count, b.seg_begin, b.rec_tmp, b.perm, b.rec,
+                                                      b.mid_list, b.huge_list, b.status, rs);
+        count_launch();
+    }
+    if (b.np > FIXREC_WARP_MAX) {
+        if ((e = cudaFuncSetAttribute(k_fixrec_cta, cudaFuncAttributeMaxDynamicSharedMemorySize, CTA_BIN_MAX * 8)))
+            return e;
+        k_fixrec_cta<<<148, 1024, CTA_BIN_MAX * 8, s>>>(b.count, b.seg_begin, b.rec_tmp, b.perm, b.rec, b.mid_list,
+                                                         b.status, rs);
+        count_launch();
+    }
+    if (b.np > CTA_BIN_MAX) {
+        k_fixrec_huge<<<8, 1024, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.rec_tmp, b.perm, b.rec, b.huge_list,
+                                          b.status, rs);
+        count_launch();
+    }
+    pt.mark("fixrec");
+    return cudaGetLastError();
+}
+
 cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
 {
     cudaError_t e;
@@ -921,12 +1322,23 @@ cudaError_t sort_enqueue(const Geo &geo, const SortBufs &b, cudaStream_t s)
     k_scan_add<<<nblk, SCAN_T, 0, s>>>(b.seg_begin, b.nbins, b.scan_tmp);
     count_launch(3);
     pt.mark("scan");
+    if (b.rec_tmp && b.np > 0)
+        return recfirst_enqueue(geo, b, s, pt);
     if (b.np > 0) {
         k_place<<<blocks_for((b.np + 3) / 4, T), T, 0, s>>>(b.np, b.key, b.rank, b.seg_begin, b.perm);
         count_launch();
         pt.mark("place");
     }
     return fixup_scatter_enqueue(geo, b, s, pt);
+}
+
+cudaError_t inverse_enqueue(const int32_t *perm, const int32_t *seg_end, int64_t capacity, int32_t *dest,
+                            cudaStream_t s)
+{
+    const int64_t want = (capacity + 255) / 256;
+    k_inverse<<<(unsigned)(want < 148 * 16 ? (want < 1 ? 1 : want) : 148 * 16), 256, 0, s>>>(perm, seg_end, dest);
+    count_launch();
+    return cudaGetLastError();
 }
 
 cudaError_t resort_enqueue(const Geo &geo, const SortBufs &b, const IncBufs &ib, cudaStream_t s)
