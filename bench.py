@@ -66,6 +66,13 @@ def alg_bytes_per_particle(order, ncomp, ppc):
     return (HBM_BYTES_PER_PARTICLE_IN if ncomp == 9 else 32.0) + S * ncomp * 8.0 / ppc
 
 
+def sort_path(np_):
+    """Which sort pipeline libmm takes for np_ particles (include/mm.h)."""
+    thr = int(os.environ.get("MM_SORT_RECFIRST_MIN", 48_000_000))
+    return ("record-first (k_key, scan, k_scatter0, k_fixrec)" if np_ >= thr
+            else "classic (k_key, scan, k_place, k_fix, k_scatter)")
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -579,6 +586,7 @@ def main():
                           "assemble_alone_ms": r1.get("assemble_alone_ms"),
                           "serial_step_ms": (r1.get("sort_ms") or 0) + (r1.get("assemble_alone_ms") or 0),
                           "sort_ms": r1.get("sort_ms"), "sort_async_ms": r1.get("sort_async_ms"),
+                          "sort_path": sort_path(r1["np"]),
                           "step_sort": "mm_sort_by_cell" if args.sync_sort else "mm_sort_by_cell_async + mm_sort_wait",
                           "assemble_ms": r1["assemble_ms"],
                           "sort_nearly_sorted_input_ms": sort_nearly_ms,
@@ -764,7 +772,8 @@ def main():
             ent = {"workload": f"{name}: 128^3, clustered double-Harris-like ppc (mean {ppc4:.2f}), "
                                f"{'CIC' if order == 1 else 'TSC'}, scalar FP64 mass matrix",
                    "particles": np4, "value": np4 / ((t_sort + t_asm) / 1e3) / 1e6, "unit": UNIT,
-                   "ms_per_step": t_sort + t_asm, "sort_ms": t_sort, "assemble_ms": t_asm,
+                   "ms_per_step": t_sort + t_asm, "sort_ms": t_sort, "sort_path": sort_path(np4),
+                   "assemble_ms": t_asm,
                    "assemble_mps": np4 / (t_asm / 1e3) / 1e6, "clocks": clk4.summary()}
             hbm = np4 * B / (t_asm / 1e3) / 1e9
             tfl = np4 * F / (t_asm / 1e3) / 1e12
@@ -869,6 +878,7 @@ def main():
                                        "random B, FP64 tensor; particles drawn on the device (synth.particles_device)",
                            "n_gpus": world, "grid": list(cfgw.n), "scaling": "weak",
                            "exchange": "NCCL send/recv inside libmm (mm_assemble_slab), self ring at N = 1",
+                           "sort_path": sort_path(int(np.prod(cfgw.n[1:])) * per * 64),
                            **weak}
         del dw
         torch.cuda.empty_cache()

@@ -14,3 +14,4 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_a
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_asm_pps" -c 1 -f -o gpurun_out/prof_c4o2 python tools/time_c4.py 2 1 > /dev/null 2>&1; echo ncu5 $?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_apply" -c 1 -f -o gpurun_out/prof_apply python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --no-tf32 --no-order2 --no-c4 > /dev/null 2>&1; echo ncu6 $?
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_moments|k_gather" -c 2 -f -o gpurun_out/prof_next4 python tools/time_next4.py > /dev/null 2>&1; echo ncu7 $?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_scatter0|k_fixrec_warp" -c 2 -f -o gpurun_out/prof_recfirst python tools/time_sort_big.py 1 > /dev/null 2>&1; echo ncu8 $?

@@ -74,7 +74,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r01")
     ap.add_argument("--src", default="gpurun_out")
-    ap.add_argument("--reps", nargs="*", default=["prof_c2", "prof_c3", "prof_tf32", "prof_c4o2", "prof_apply", "prof_sort", "prof_next4"])
+    ap.add_argument("--reps", nargs="*", default=["prof_c2", "prof_c3", "prof_tf32", "prof_c4o2", "prof_apply", "prof_sort", "prof_next4", "prof_recfirst", "prof_tp"])
     a = ap.parse_args()
     os.makedirs("profiles", exist_ok=True)
     lines = [f"# ncu summary ({a.round})", "",
