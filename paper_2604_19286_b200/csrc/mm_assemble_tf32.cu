@@ -155,7 +155,11 @@ __device__ __forceinline__ void coeff_f(float q, float Bx, float By, float Bz, f
     } else {
         const float o0 = wscale * Bx, o1 = wscale * By, o2 = wscale * Bz;
         const float d = fmaf(o0, o0, fmaf(o1, o1, fmaf(o2, o2, 1.0f)));
-        const float f = __fdiv_rn(sigma * q, d);
+        // reciprocal + one Newton step (<= 1 ulp; no division subroutine call in the prep)
+        float r;
+        asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+        r = fmaf(r, fmaf(-d, r, 1.0f), r);
+        const float f = (sigma * q) * r;
         const float f0 = f * o0, f1 = f * o1, f2 = f * o2;
         s[0] = fmaf(f0, o0, f);
         s[1] = fmaf(f0, o1, f2);
@@ -178,12 +182,14 @@ template <int ORDER>
 __device__ __forceinline__ void pair_products(double xi, float q[ORDER == 1 ? 3 : 6])
 {
     if (ORDER == 1) {
-        const float w1 = (float)xi, w0 = (float)(1.0 - xi);
+        const float w1 = (float)xi, w0 = 1.0f - w1;  // abs. error <= 2^-25 either way, off the FP64 pipe
         q[0] = w0 * w0;
         q[1] = w0 * w1;
         q[2] = w1 * w1;
     } else {
-        const float u = (float)(xi >= 0.5 ? xi - 1.0 : xi);
+        // base decided in FP64 as in the sort; the shift by one in FP32 (absolute error <= 2^-25,
+        // far below the TF32 / 3xTF32 operand rounding) keeps the subtraction off the FP64 pipe
+        const float u = xi >= 0.5 ? (float)xi - 1.0f : (float)xi;
         const float h = 0.5f - u, k = 0.5f + u;
         const float w0 = (0.5f * h) * h, w1 = fmaf(-u, u, 0.75f), w2 = (0.5f * k) * k;
         q[0] = w0 * w0;
