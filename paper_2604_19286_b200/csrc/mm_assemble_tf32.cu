@@ -15,8 +15,10 @@
 // blocks of D are unused.  The tensor work is tiny next to the HBM traffic, so the wasted
 // blocks cost nothing measurable, and the layout puts bin j's rows in TMEM lanes that its
 // own warp(s) can read (tcgen05.ld: warp w reads lanes 32 (w % 4) .. +31).
-//   order 1: BPC = 4, MB = 32, NB = 16, N = 64   (warp j = bin j)
-//   order 2: BPC = 2, MB = 64, NB = 64, N = 128
+//   order 1:         BPC = 4, MB = 32, NB = 16, N = 64    (warp j = bin j)
+//   order 2 scalar:  BPC = 4, MB = 32, NB = 48, N = 192   (6 Z rows per bin: two warps per bin
+//                    amortise the per-chunk overhead over twice the rows of the 4-warp layout)
+//   order 2 tensor:  BPC = 2, MB = 64, NB = 64, N = 128
 // 8 warps per CTA: each bin has 2 (order 1) or 4 (order 2) warps that split its X / Z rows in
 // the prep and its entries in the deposit; warps 0-3 read the accumulators (lane quarter = warp).
 // Per 32-particle chunk: prep (FP32 from the FP64 record; the support base is decided in FP64
@@ -206,10 +208,10 @@ struct PP {
     static constexpr int NU = ORDER == 1 ? 3 : 6;      // pair products per axis
     static constexpr int NX = NU * NU;                  // X rows: 9 | 36
     static constexpr int NZ = NU * NC;                  // Z rows: 27 | 3 | 54 | 6
-    static constexpr int BPC = ORDER == 1 ? 4 : 2;      // bins per CTA group
+    static constexpr int BPC = (ORDER == 1 || NC == 1) ? 4 : 2;  // bins per CTA group
     static constexpr int THREADS = 256, WPB = 8 / BPC;  // warps per bin
     static constexpr int MB = 128 / BPC;                // A (Z) rows per bin
-    static constexpr int NB = ORDER == 1 ? 16 : 64;     // B (X) rows per bin
+    static constexpr int NB = ORDER == 1 ? 16 : (NC == 1 ? 48 : 64);  // B (X) rows per bin
     static constexpr int N = BPC * NB;                  // MMA N: 64 | 128
     static_assert(NZ <= MB && NX <= NB, "bin block does not fit");
     static constexpr int CH = 32;                       // particles per chunk (4 K-steps of 8)
@@ -232,7 +234,7 @@ struct PP {
     static constexpr int OFF_ROWP = (OFF_TAB + TAB_BYTES + 15) / 16 * 16;
     static constexpr int OFF_BAR = OFF_ROWP + BPC * 32 * 8;
     static constexpr int SMEM = OFF_BAR + 16 * 8;
-    static constexpr int TMEM_COLS = N;
+    static constexpr int TMEM_COLS = N <= 64 ? 64 : (N <= 128 ? 128 : 256);  // power of two >= N
 };
 
 // Prep of one warp's share [R0, R1) of a bin's operand rows (X rows, then Z rows; lane = particle
@@ -367,8 +369,8 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
     // prep role of this warp: bin pj, an equal share [r0, r1) of its operand rows (X rows, then
     // Z rows).  order 1: bin j = warps j, 4+j; order 2: bin j = warps {2j, 2j+1, 2j+4, 2j+5}, so
     // warps 0-3 can read bin j's TMEM lane quarters (tcgen05.ld: warp w reads quarter w % 4).
-    const int pj = ORDER == 1 ? (warp & 3) : ((warp >> 1) & 1);
-    const int role = ORDER == 1 ? (warp >> 2) : ((warp & 1) + 2 * (warp >> 2));
+    const int pj = T::BPC == 4 ? (warp & 3) : ((warp >> 1) & 1);
+    const int role = T::BPC == 4 ? (warp >> 2) : ((warp & 1) + 2 * (warp >> 2));
 
 
     // Each bin slot pj (its 2 | 4 warps) runs independently: its own bins (group grp, slot pj),
@@ -478,7 +480,7 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             ++bc;
             tc_fence_after();
             if (warp < 4) {
-                const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
+                const int z = T::BPC == 4 ? lane : 32 * (warp & 1) + lane;
                 float *dp = dblk + (int64_t)bin * (T::NX * T::NZ);
                 const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
 #pragma unroll
@@ -517,7 +519,7 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
         ++bc;
         tc_fence_after();
         if (warp < 4) {  // lane quarter = warp: this slot's Z rows
-            const int z = ORDER == 1 ? lane : 32 * (warp & 1) + lane;
+            const int z = T::BPC == 4 ? lane : 32 * (warp & 1) + lane;
             float *ep = epi + pj * T::NX * T::NZ;
             const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16) + T::NB * pj;
 #pragma unroll
