@@ -1,0 +1,3 @@
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+for L in libmm libmm_u4 libmm libmm_u4; do timeout 300 python tools/time_variant2.py paper_2604_19286_b200/$L.so c2 2>&1 | tail -1; done
+for L in libmm libmm_u4; do MM_O1T_MINB=6 timeout 300 python tools/time_variant2.py paper_2604_19286_b200/$L.so c2 2>&1 | tail -1; done
