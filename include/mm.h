@@ -129,6 +129,11 @@ typedef struct {
  *
  * Ownership: the handle owns a sorted, padded copy of the particle data, so
  * the caller may free pos/q/B after the call.  Release with mm_free().
+ * Pipeline: from MM_SORT_RECFIRST_MIN particles on (environment, read per call;
+ * default 48e6, where the arrays exceed L2) the records are scattered first to
+ * unstable slots and put in stable order per bin (one random pass instead of
+ * three; the handle then holds an extra [capacity][8] FP64 scratch buffer).
+ * Both pipelines give bit-identical results.
  * Synchronisation: the call enqueues its kernels on `stream` and then waits
  * for that stream once, to read back the error flags (MM_ERR_DOMAIN for a
  * particle whose cell is outside [x_begin,x_end) x [0,n1) x [0,n2) — never
