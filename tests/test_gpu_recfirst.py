@@ -133,3 +133,31 @@ def test_recfirst_c2_full_equals_classic(monkeypatch):
     for k in ("seg_count", "seg_begin", "perm"):
         assert (v1[k] == v0[k]).all(), k
     assert (v1["rec"].view(np.uint64) == v0["rec"].view(np.uint64)).all()
+
+
+@pytest.mark.parametrize("bad,status", [("domain_hi", 2), ("domain_lo", 2), ("nan_pos", 3), ("inf_q", 3),
+                                        ("nan_B", 3)])
+def test_recfirst_errors(bad, status):
+    # the status words are raised by k_key (domain, positions) and k_scatter0 (q, B) as on the
+    # classic path; the asynchronous variant reports them at mm_sort_wait
+    m = mm()
+    n = (5, 5, 5)
+    d = {k: v.copy() for k, v in synth.particles(synth.Config("t", n, 1, "tensor", 4, seed=1)).items()}
+    if bad == "domain_hi":
+        d["pos"][7, 1] = 5.0
+    elif bad == "domain_lo":
+        d["pos"][3, 2] = -1e-9
+    elif bad == "nan_pos":
+        d["pos"][9, 0] = np.nan
+    elif bad == "inf_q":
+        d["q"][2] = np.inf
+    else:
+        d["B"][5, 2] = np.nan
+    dd = to_dev(d)
+    with pytest.raises(m.MMError) as e:
+        m.mm_sort_by_cell(m.Grid(n), 1, 4, dd["pos"], dd["q"], dd["B"])
+    assert e.value.status == status
+    h = m.mm_sort_by_cell(m.Grid(n), 1, 4, dd["pos"], dd["q"], dd["B"], wait=False)
+    with pytest.raises(m.MMError) as e:
+        m.mm_sort_wait(h)
+    assert e.value.status == status
