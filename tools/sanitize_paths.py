@@ -6,8 +6,10 @@ synccheck, initcheck).  No oracle, no timing: the sanitizer reports are the prod
 c1: BASELINE.json configs[0] (4^3, 16 ppc); small: 12 x 10 x 9 grid, 40 ppc (several chunks per
 bin, several bins per CTA / warp, slab grids with ghost planes).
 """
+import os
 import sys
 
+import numpy as np
 import torch
 
 sys.path.insert(0, ".")
@@ -63,8 +65,36 @@ def main(which="small"):
             else:
                 mm.mm_slab_partition(g, dd["pos"], dd["q"], dd["B"])
             torch.cuda.synchronize()
-            mm.mm_free(h)
-            mm.mm_free(hs)
+            # record-first sort (k_scatter0 / k_fixrec_*) and the two-phase deposit (k_nodesum)
+            os.environ["MM_SORT_RECFIRST_MIN"] = "1"
+            hr = mm.mm_sort_by_cell(g, order, 4, dd["pos"], dd["q"], dd["B"])
+            hrs = mm.mm_sort_by_cell(g, order, 4, dd["pos"], dd["q"], None)
+            os.environ["MM_TWO_PHASE"] = "7"
+            for kind, hh in ((mm.MM_TENSOR, hr), (mm.MM_SCALAR, hrs)):
+                for prec in (mm.MM_FP64, mm.MM_TF32):
+                    dt = torch.float64 if prec == mm.MM_FP64 else torch.float32
+                    out = torch.empty(mm.out_shape(g, order, kind), dtype=dt, device="cuda")
+                    ghost = torch.empty(mm.ghost_shape(g, order, kind), dtype=dt, device="cuda") if slab else None
+                    mm.mm_assemble(hh, kind, prec, sp, out, ghost)
+                    torch.cuda.synchronize()
+            os.environ.pop("MM_TWO_PHASE")
+            if not slab:
+                mm.mm_resort_by_cell(hr, dd["pos"], dd["q"], dd["B"])  # rebuilds the inverse permutation
+            torch.cuda.synchronize()
+            os.environ.pop("MM_SORT_RECFIRST_MIN")
+            for x in (h, hs, hr, hrs):
+                mm.mm_free(x)
+    # record-first fix-up of a bin beyond the warp path (k_fixrec_cta) and beyond CTA_BIN_MAX
+    # (k_fixrec_huge)
+    os.environ["MM_SORT_RECFIRST_MIN"] = "1"
+    for npart in (700, 17000):
+        rng = np.random.default_rng(npart)
+        pos = torch.from_numpy(np.array([2.0, 3.0, 1.0]) + rng.random((npart, 3)) * 0.999).cuda()
+        q = torch.from_numpy(rng.uniform(0.5, 1.5, npart)).cuda()
+        hb = mm.mm_sort_by_cell(mm.Grid((5, 5, 5)), 1, 4, pos, q, None)
+        torch.cuda.synchronize()
+        mm.mm_free(hb)
+    os.environ.pop("MM_SORT_RECFIRST_MIN")
     print("sanitize paths done", which)
 
 
