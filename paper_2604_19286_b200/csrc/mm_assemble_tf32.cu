@@ -242,8 +242,8 @@ struct PP {
 // tiles as TF32: element (row m, k) at (m >> 3) 1024 + (m & 7) 128 + ((k >> 2) ^ (m & 7)) 16 +
 // (k & 3) 4.  For a fixed row the 32 lanes hit 32 distinct banks (no staging round trip).
 template <int ORDER, int NC, bool X3, int ROLE>
-__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, unsigned char *op, int pj,
-                                          const uint32_t (&lo8)[8], float fws, float fsig)
+__device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, bool live, uint32_t opb, int pj,
+                                          uint32_t bl, float fws, float fsig)
 {
     using T = PP<ORDER, NC, X3>;
     if constexpr (ROLE >= T::WPB) {
@@ -269,26 +269,28 @@ __device__ __forceinline__ void prep_tile(const double4 &ca, const double4 &cb, 
             coeff_f<NC>((float)ca.w, (float)cb.x, (float)cb.y, (float)cb.z, fws, fsig, sc);
         }
     }
-    // tile row m = NB pj + r (X) | MB pj + r - NX (Z): m & 7 is a compile-time constant, so the
-    // rows are visited grouped by their swizzle phase and each lane offset lo8[m & 7] is used
-    // from one register at a time; m >> 3 splits into a per-slot base plus a constant
-    unsigned char *base_x = op + T::A_BYTES + (T::NB / 8 * pj) * 1024;
-    unsigned char *base_z = op + (T::MB / 8 * pj) * 1024;
+    // tile row m = NB pj + r (X) | MB pj + r - NX (Z), m & 7 a compile-time constant.  The
+    // per-slot tile bases are 1024-B aligned, so base | bl (bl = the lane's (k >> 2) 16 + (k & 3) 4)
+    // XOR (m & 7) 16 is the swizzled lane offset of the row's phase: ONE LOP3 per phase and X | Z
+    // block, the row's atom and phase offsets ((m >> 3) 1024 + (m & 7) 128) are store immediates
+    const uint32_t bx = (opb + T::A_BYTES + (T::NB / 8 * pj) * 1024) | bl;
+    const uint32_t bz = (opb + (T::MB / 8 * pj) * 1024) | bl;
 #pragma unroll
     for (int r7 = 0; r7 < 8; ++r7) {
-        // one register base per (swizzle phase, X | Z block); the row's atom offset is an immediate
-        unsigned char *lx = base_x + lo8[r7], *lz = base_z + lo8[r7];
+        const uint32_t lx = bx ^ (uint32_t)(r7 << 4), lz = bz ^ (uint32_t)(r7 << 4);
 #pragma unroll
         for (int r = R0; r < R1; ++r) {
             const int mr = r < T::NX ? r : r - T::NX;  // row inside the bin's X or Z block
             if ((mr & 7) != r7)
                 continue;
             const float v = r < T::NX ? qx[r / T::NU] * qy[r % T::NU] : qz[(r - T::NX) / NC] * sc[(r - T::NX) % NC];
-            unsigned char *d = (r < T::NX ? lx : lz) + (mr >> 3) * 1024;
+            const uint32_t d = (r < T::NX ? lx : lz) + (uint32_t)((mr >> 3) * 1024 + r7 * 128);
             const uint32_t hi = tf32_rna(v);
-            *reinterpret_cast<uint32_t *>(d) = hi;
+            asm volatile("st.shared.b32 [%0], %1;" ::"r"(d), "r"(hi) : "memory");
             if (X3)
-                *reinterpret_cast<uint32_t *>(d + T::PART_BYTES) = tf32_rna(v - __uint_as_float(hi));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(d + (uint32_t)T::PART_BYTES),
+                             "r"(tf32_rna(v - __uint_as_float(hi)))
+                             : "memory");
         }
     }
     }
@@ -379,11 +381,8 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
     // slots' rows (possibly while they are rewritten), which only produce D lanes outside its
     // quarter(s), never read.
     const int pthreads = 32 * T::WPB;
-    // lane part of the swizzled tile offset for each value of (row & 7) (see prep_tile)
-    uint32_t lo8[8];
-#pragma unroll
-    for (int r7 = 0; r7 < 8; ++r7)
-        lo8[r7] = (uint32_t)((((lane >> 2) ^ r7) << 4) + (lane & 3) * 4 + r7 * 128);
+    // lane part of the swizzled tile offset before the row-phase XOR (see prep_tile)
+    const uint32_t bl = (uint32_t)(((lane >> 2) << 4) | ((lane & 3) << 2));
     const bool issuer = role == 0 && lane == 0;
     static_assert(T::CH == 32, "4 K-steps per chunk");
     uint64_t *bar_buf = bar + 2 * pj, *bar_acc = bar + 2 * T::BPC + pj;
@@ -430,10 +429,10 @@ __global__ void __launch_bounds__(256, ORDER == 1 ? 3 : 2) k_asm_tf32(Geo g, con
             {
                 const bool live = T::CH * c + lane < nb;
                 switch (role) {
-                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, op, pj, lo8, fws, fsig); break;
-                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, op, pj, lo8, fws, fsig); break;
-                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, op, pj, lo8, fws, fsig); break;
-                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, op, pj, lo8, fws, fsig); break;
+                case 0: prep_tile<ORDER, NC, X3, 0>(ca, cb, live, smem_u32(op), pj, bl, fws, fsig); break;
+                case 1: prep_tile<ORDER, NC, X3, 1>(ca, cb, live, smem_u32(op), pj, bl, fws, fsig); break;
+                case 2: prep_tile<ORDER, NC, X3, 2>(ca, cb, live, smem_u32(op), pj, bl, fws, fsig); break;
+                default: prep_tile<ORDER, NC, X3, 3>(ca, cb, live, smem_u32(op), pj, bl, fws, fsig); break;
                 }
             }
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
