@@ -146,6 +146,73 @@ __global__ void k_batch(int iters, double *sink)
         sink[threadIdx.x] = s;
 }
 
+// tcgen05 TF32 peak: one thread per CTA issues back-to-back tcgen05.mma kind::tf32 (M = 128,
+// N = 256, K = 8) from two 128-B-swizzled K-major smem tiles (contents irrelevant) into TMEM,
+// `iters` x 4 K-steps, then one commit; the CTA waits on the mbarrier.  FLOPs per MMA =
+// 2 x 128 x 256 x 8.  (The TF32 roofline denominator the north_star asks for.)
+__device__ __forceinline__ uint32_t p_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__global__ void __launch_bounds__(128, 1) k_tf32_mma(int iters, double *sink)
+{
+    extern __shared__ __align__(1024) unsigned char psm[];
+    unsigned char *A = psm, *B = psm + 128 * 128;  // A: 128 rows x 128 B, B: 256 rows x 128 B
+    __shared__ uint64_t bar;
+    __shared__ uint32_t taddr;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < (128 + 256) * 128 / 4; i += blockDim.x)
+        reinterpret_cast<uint32_t *>(psm)[i] = 0x3f800000u ^ (uint32_t)(i & 0xff);
+    if (tid == 0)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(p_smem_u32(&bar)) : "memory");
+    if (tid < 32) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(p_smem_u32(&taddr))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = taddr;
+    if (tid == 0) {
+        auto desc = [](uint32_t a) {
+            return ((uint64_t)(a >> 4) & 0x3FFFull) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+                   (1ull << 46) | (2ull << 61);
+        };
+        const uint64_t dA = desc(p_smem_u32(A)), dB = desc(p_smem_u32(B));
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        for (int it = 0; it < iters; ++it) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+                const uint32_t acc = (it > 0 || ks > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+                    "l"(dA + 2 * ks), "l"(dB + 2 * ks), "r"(idesc), "r"(acc)
+                    : "memory");
+            }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         p_smem_u32(&bar))
+                     : "memory");
+    }
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t@!p bra W_%=;\n\t}" ::"r"(p_smem_u32(&bar))
+        : "memory");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    uint32_t v;
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(tmem + ((32u * (tid >> 5)) << 16)));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (v == 0x12345678u)
+        sink[tid] = (double)v;
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (tid < 32)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+}
+
 __global__ void k_copy(const double4 *__restrict__ a, double4 *__restrict__ b, int64_t n)
 {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -204,6 +271,15 @@ float probe_red(double *buf, int64_t nelem, int blocks, int threads, int per_war
 float probe_batch(int blocks, int iters, double *sink)
 {
     return timed([&] { k_batch<<<blocks, 256>>>(iters, sink); });
+}
+
+// TF32 flops = blocks * iters * 4 * 2 * 128 * 256 * 8  (one CTA per SM)
+float probe_tf32(int blocks, int iters, double *sink)
+{
+    const int smem = (128 + 256) * 128;
+    if (cudaFuncSetAttribute(k_tf32_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return -1.f;
+    return timed([&] { k_tf32_mma<<<blocks, 128, smem>>>(iters, sink); });
 }
 
 // bytes = 2 * n4 * 32

@@ -25,7 +25,7 @@ def main():
     lib = ctypes.CDLL(_build.PROBE_LIB)
     F, P, I, I64 = ctypes.c_float, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
     for nm, at in (("probe_batch", [I, I, P]), ("probe_dmma", [I, I, I, P]), ("probe_dfma", [I, I, I, P]), ("probe_mixed", [I, I, I, P]),
-                   ("probe_red", [P, I64, I, I, I, I]), ("probe_copy", [P, P, I64])):
+                   ("probe_red", [P, I64, I, I, I, I]), ("probe_copy", [P, P, I64]), ("probe_tf32", [I, I, P])):
         getattr(lib, nm).argtypes = at
         getattr(lib, nm).restype = F
     sink = torch.zeros(1024, dtype=torch.float64, device="cuda")
@@ -56,6 +56,12 @@ def main():
         ms = lib.probe_batch(b, 500, sp)
         fl = b * 8 * 500 * 8 * 9 * 512
         res["batch_loop"].append({"ctas_per_sm": bps, "dmma_tflops": fl / ms / 1e9})
+    # tcgen05 kind::tf32 (M 128, N 256, K 8) issued back to back by one thread per SM
+    tf = []
+    for iters in (2000, 8000):
+        ms = lib.probe_tf32(sms, iters, sp)
+        tf.append(sms * iters * 4 * 2 * 128 * 256 * 8 / ms / 1e9 if ms > 0 else None)
+    res["tf32_tcgen05_tflops"] = max(t for t in tf if t) if any(tf) else None
     res["dmma_tflops"] = best["dmma"]
     res["dfma_tflops"] = best["dfma"]
     res["mixed_tflops"] = best["mixed"]
