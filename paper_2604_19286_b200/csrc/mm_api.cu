@@ -699,7 +699,7 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
         }
         // the work counter is read only by the ticket-scheduled kernels (k_asm_o2t, and k_asm_o1t
         // with in-kernel zeroing); the others use a static schedule
-        if (zflags || (prec == MM_FP64 && h->order == 2 && kind == MM_TENSOR)) {
+        if (zflags || (prec == MM_FP64 && kind == MM_TENSOR)) {
             e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
             if (e)
                 return cuda_fail(e, "mm_assemble memset");

@@ -29,16 +29,24 @@
 // sums of a node-a term and a (b, c) term (slot(b - a) = 13 + sb(b) - sa(a), stage = ka(a) +
 // kb(b) + c), so lane p holds the (b, c) terms of p, p + 32 and 64 + (p & 7) and the a terms
 // are compile-time offsets / one shared row pointer: 18 REDs of 32 lanes per bin, ~4
-// instructions each.  Bins are taken in DESCENDING order from a ticket counter (one per warp
-// and bin); the output is zeroed inside the kernel, row by row, by the first-writer scheme
-// of mm_device.cuh (no memset pass, rows zeroed in L2 just before their REDs).  Records are
-// read with an L2 evict-first hint (streamed once), so the 126 MB L2 keeps node rows.
+// instructions each.  Bins are taken in DESCENDING order from a work counter, a warp drawing
+// runs of O1T_DYN consecutive tickets with one atomic (dynamic balance across the SMs, and the
+// run's z-adjacent bins share half their node rows in L2); with MM_ZERO_O1 the output is zeroed
+// inside the kernel, row by row, by the first-writer scheme of mm_device.cuh (one ticket per
+// bin).  Records are read with an L2 evict-first hint (streamed once), so the 126 MB L2 keeps
+// node rows.
 #include <cstdlib>
 
 #include "mm_device.cuh"
 
 #ifndef O1T_UNROLL
 #define O1T_UNROLL 4  // full chunks run the 4 batch pairs unrolled (0.683 -> 0.678 ms at c2); 1: rolled loop
+#endif
+
+#ifndef O1T_DYN
+#define O1T_DYN 8  // bins from the work counter in runs of 8 tickets (c2 0.680 -> 0.653 ms incl. the
+                   // zero-fill against the static interleaved schedule; runs of 1: 1.47 ms, the
+                   // single counter serialises; 2: 0.97, 4: 0.70, 16: 0.653, 32: 0.667); 0: static
 #endif
 
 #ifndef O1T_MINB
@@ -66,6 +74,7 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
               double sigma, double *__restrict__ out, double *__restrict__ ghost, int *__restrict__ work, ZeroPlan zp)
 {
     using L = O1T;
+    constexpr bool TICKET = ZERO || O1T_DYN > 0;  // bins from the work counter
     extern __shared__ __align__(16) double dsm_o1t[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double *xz = dsm_o1t + warp * L::WD;
@@ -102,14 +111,26 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
     // tickets: cur (this bin) and nxt, in processing order; bin = nbins - 1 - ticket.  A
     // ticket's zero task (mm_device.cuh) runs as soon as the ticket is known: lanes lbase..+7
     // get the rows of ticket + D, lanes lbase+8..+15 the own rows of a ticket < D.
-    // ZERO: tickets from the work counter (first-writer zeroing needs them); else the static
-    // interleaved schedule (warp w: tickets w, w + W, ...)
+    // ZERO: one ticket per bin from the work counter (the first-writer zeroing needs them);
+    // O1T_DYN > 0: runs of O1T_DYN tickets per atomic; O1T_DYN = 0: the static interleaved
+    // schedule (warp w: tickets w, w + W, ...)
     const int W = gridDim.x * L::WARPS;
     int cur = blockIdx.x * L::WARPS + warp, nxt = cur + W;
-    if (ZERO) {
+    // O1T_DYN: lane 0 draws runs of O1T_DYN consecutive tickets with one atomic (tk .. tk_end)
+    int tk = 0, tk_end = 0;
+    auto next_ticket = [&]() {
+        if (ZERO)
+            return ticket(work);
+        if (tk == tk_end) {
+            tk = atomicAdd(work, O1T_DYN > 0 ? O1T_DYN : 1);
+            tk_end = tk + (O1T_DYN > 0 ? O1T_DYN : 1);
+        }
+        return tk++;
+    };
+    if (TICKET) {
         if (lane == 0) {
-            cur = ticket(work);
-            nxt = ticket(work);
+            cur = next_ticket();
+            nxt = next_ticket();
         }
         cur = __shfl_sync(0xffffffffu, cur, 0);
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
@@ -117,7 +138,7 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
     // bin coordinates (bin plane x, y, z) of the static schedule, stepped by the mixed-radix
     // digits of W instead of two integer divisions per bin
     int cx = 0, cy = 0, cz = 0, wx = 0, wy = 0, wz = 0;
-    if (!ZERO) {
+    if (!TICKET) {
         wz = W % g.n2;
         wy = (W / g.n2) % g.n1;
         wx = W / plane;
@@ -158,11 +179,11 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
     __syncwarp();
     while (cur < nbins) {
         int nn = nxt + W;
-        if (ZERO && lane == 0)
-            nn = ticket(work);  // consumed at the end of this bin
+        if (TICKET && lane == 0)
+            nn = next_ticket();  // consumed at the end of this bin
         const int bin = nbins - 1 - cur;
         int bxl = cx, by = cy, bz = cz;
-        if (ZERO) {
+        if (TICKET) {
             bxl = bin / plane;
             const int rem = bin - bxl * plane;
             by = rem / g.n2;
@@ -308,13 +329,13 @@ __global__ void __launch_bounds__(O1T::WARPS * 32, MINB)
                 rb = ld256_ef(rec + 8 * (int64_t)(nb0 + lane) + 4);
             }
         }
-        if (ZERO) {
+        if (TICKET)
             nn = __shfl_sync(0xffffffffu, nn, 0);
-            zero_task(nn, 0);
-        }  // rel is free: released above (or still pending for an empty bin)
+        if (ZERO)
+            zero_task(nn, 0);  // rel is free: released above (or still pending for an empty bin)
         cur = nxt;
         nxt = nn;
-        if (!ZERO) {  // bin - W
+        if (!TICKET) {  // bin - W
             cz -= wz;
             if (cz < 0) {
                 cz += g.n2;
