@@ -697,9 +697,9 @@ mm_status mm_assemble(const mm_sorted *h, mm_kind kind, mm_precision prec, const
             if (e)
                 return cuda_fail(e, "mm_assemble memset");
         }
-        // the work counter is read only by the ticket-scheduled kernels (k_asm_o2t, and k_asm_o1t
-        // with in-kernel zeroing); the others use a static schedule
-        if (zflags || (prec == MM_FP64 && kind == MM_TENSOR)) {
+        // the work counter is read by the ticket-scheduled FP64 kernels (runs of bins per atomic);
+        // the TF32 kernels use a static schedule
+        if (zflags || prec == MM_FP64) {
             e = cudaMemsetAsync(h->d_work, 0, sizeof(int32_t) * 4, s);
             if (e)
                 return cuda_fail(e, "mm_assemble memset");

@@ -19,6 +19,16 @@
 
 #include "mm_device.cuh"
 
+#ifndef O2T_DYN
+#define O2T_DYN 4  // k_asm_o2t: tickets per atomic, runs of consecutive bins per CTA (c3 4.537 ->
+                   // 4.474 ms incl. the zero-fill; runs of 2: 4.491)
+#endif
+
+#ifndef PPS_DYN
+#define PPS_DYN 8  // scalar kernels take bins from the work counter in runs of 8 (c4o1 2.05 -> 1.95 ms,
+                   // c4o2 6.41 -> 6.32; runs of 4: 2.47 / 6.29, 16: 1.99 / 6.39); 0: static schedule
+#endif
+
 namespace mm {
 
 namespace {
@@ -140,10 +150,19 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
             m54[by] = 54 * (6 * px + ay + by + (ay && by));
         s_unit[u] = make_int4(a, slot * 9, m54[0] | (m54[1] << 16), m54[2] | (az << 16));
     }
+    // O2T_DYN: thread 0 draws runs of O2T_DYN consecutive tickets with one atomic
+    int tk = 0, tk_end = 0;
+    auto next_ticket = [&]() {
+        if (tk == tk_end) {
+            tk = atomicAdd(work, O2T_DYN);
+            tk_end = tk + O2T_DYN;
+        }
+        return tk++;
+    };
     if (threadIdx.x == 0) {
-        q[0] = atom_add(work, 1);
-        q[1] = atom_add(work, 1);
-        q[2] = atom_add(work, 1);
+        q[0] = next_ticket();
+        q[1] = next_ticket();
+        q[2] = next_ticket();
         q[3] = -1;
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
@@ -269,7 +288,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
                 q[0] = q[1];
                 q[1] = q[2];
                 if (q[2] < nbins)
-                    q[2] = atom_add(work, 1);
+                    q[2] = next_ticket();
             }
             __syncthreads();
             bin = q[0];
@@ -302,7 +321,7 @@ __global__ void __launch_bounds__(O2T::WARPS * 32, 4) k_asm_o2t(Geo g, const dou
             q[0] = q[1];
             q[1] = q[2];
             if (q[2] < nbins)
-                q[2] = atom_add(work, 1);
+                q[2] = next_ticket();
         }
         __syncthreads();
         bin = q[0];
@@ -364,7 +383,8 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                                                                    int64_t nbins, int rs, double sigma,
                                                                    double *__restrict__ out,
                                                                    double *__restrict__ ghost,
-                                                                   double *__restrict__ dblk)
+                                                                   double *__restrict__ dblk,
+                                                                   int *__restrict__ work)
 {
     using L = PPS<ORDER>;
     extern __shared__ __align__(16) double dsm_pps[];
@@ -403,15 +423,32 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
     __syncthreads();
 
     const int nw = gridDim.x * L::WARPS;
-    int bin = blockIdx.x * L::WARPS + warp;
+    // PPS_DYN > 0: bins from the work counter, a warp drawing runs of PPS_DYN consecutive bins
+    // with one atomic (lane 0); else the static interleaved schedule (warp w: w, w + nw, ...)
+    int tk = 0, tk_end = 0;
+    auto next_bin_of = [&](int static_next) {
+        if (PPS_DYN == 0)
+            return static_next;
+        int t = 0;
+        if (lane == 0) {
+            if (tk == tk_end) {
+                tk = atomicAdd(work, PPS_DYN > 0 ? PPS_DYN : 1);
+                tk_end = tk + (PPS_DYN > 0 ? PPS_DYN : 1);
+            }
+            t = tk++;
+        }
+        return __shfl_sync(0xffffffffu, t, 0);
+    };
+    int bin = next_bin_of(blockIdx.x * L::WARPS + warp);
+    int bnext = next_bin_of(bin + nw);
     int b0 = 0, b1 = 0, nb0 = 0, nb1 = 0;
     if (bin < nbins) {
         b0 = __ldg(seg_begin + bin);
         b1 = __ldg(seg_begin + bin + 1);
     }
-    if (bin + nw < nbins) {
-        nb0 = __ldg(seg_begin + bin + nw);
-        nb1 = __ldg(seg_begin + bin + nw + 1);
+    if (bnext < nbins) {
+        nb0 = __ldg(seg_begin + bnext);
+        nb1 = __ldg(seg_begin + bnext + 1);
     }
     double4 ra = make_double4(0, 0, 0, 0);
     if (bin < nbins && b0 + lane < b1)
@@ -423,10 +460,16 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
     const int wz = nw % g.n2, wy = (nw / g.n2) % g.n1, wx = nw / plane;
     int cx = bin / plane, cy = (bin - cx * plane) / g.n2, cz = bin - cx * plane - cy * g.n2;
     while (bin < nbins) {
+        const int bnn = next_bin_of(bnext + nw);
         int nn0 = 0, nn1 = 0;
-        if (bin + 2 * nw < nbins) {
-            nn0 = __ldg(seg_begin + bin + 2 * nw);
-            nn1 = __ldg(seg_begin + bin + 2 * nw + 1);
+        if (bnn < nbins) {
+            nn0 = __ldg(seg_begin + bnn);
+            nn1 = __ldg(seg_begin + bnn + 1);
+        }
+        if (PPS_DYN > 0) {
+            cx = bin / plane;
+            cy = (bin - cx * plane) / g.n2;
+            cz = bin - cx * plane - cy * g.n2;
         }
         double acc[L::MT][2];
 #pragma unroll
@@ -440,7 +483,7 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                 if (base + 32 < b1) {
                     if (base + 32 + lane < b1)
                         p = base + 32 + lane;
-                } else if (bin + nw < nbins && nb0 + lane < nb1) {
+                } else if (bnext < nbins && nb0 + lane < nb1) {
                     p = nb0 + lane;
                 }
                 if (p >= 0)
@@ -542,11 +585,12 @@ __global__ void __launch_bounds__(PPS<ORDER>::WARPS * 32) k_asm_pps(Geo g, const
                 for (int e = lane; e < L::NX * L::NZ; e += 32)
                     dp[e] = 0.0;
             }
-            if (bin + nw < nbins && nb0 + lane < nb1)
+            if (bnext < nbins && nb0 + lane < nb1)
                 ra = ld256(rec + rs * (int64_t)(nb0 + lane));
         }
     next_bin:
-        bin += nw;
+        bin = bnext;
+        bnext = bnn;
         cz += wz;
         if (cz >= g.n2) {
             cz -= g.n2;
@@ -582,7 +626,7 @@ cudaError_t launch_pps(const Geo &geo, const AsmArgs &a, cudaStream_t s)
     int64_t cap = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
     unsigned grid = (unsigned)(want < cap ? (want < 1 ? 1 : want) : cap);
     k_asm_pps<ORDER><<<grid, L::WARPS * 32, L::SMEM, s>>>(geo, a.rec, a.seg_begin, a.nbins, a.rec_stride, a.sigma,
-                                                          a.out, a.ghost, static_cast<double *>(a.dblk));
+                                                          a.out, a.ghost, static_cast<double *>(a.dblk), a.work);
     count_launch();
     return cudaGetLastError();
 }
